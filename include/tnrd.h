@@ -1,0 +1,147 @@
+/*
+ * tnrd.h -- C ABI of the B200-native TNRD despeckling inference path.
+ *
+ * The reference (specklediff, pure Python) has no FFI; its "operator API" is
+ * the Python function set below.  Each entry point here is what a binding of
+ * that function would call (the ctypes binding lives in
+ * paper_1702_07482_b200/_lib.py).  Reference paths are
+ * relative to /root/reference/pkg/src/specklediff.
+ *
+ *   tnrd_model_create     <- DiffusionModel + StageParams (diffusion.py:46-130)
+ *                            parameters uploaded once; kernels are the
+ *                            reference's k_i = coeffs @ basis.T (diffusion.py:76-77)
+ *   tnrd_despeckle        <- run_diffusion            (diffusion.py:227-242)
+ *   tnrd_stage            <- diffusion_step           (diffusion.py:184-194)
+ *                            (and diffusion_force, diffusion.py:171-181, with
+ *                            TNRD_STAGE_FORCE)
+ *   tnrd_plan_*_host      <- run_diffusion called with host arrays (the
+ *                            reference's only calling convention)
+ *   tnrd_conv2d           <- conv2d                   (imageops.py:53-72)
+ *   tnrd_prox_idiv        <- prox_idiv                (speckle.py:111-121)
+ *
+ * Conventions
+ *   - images are fp32, row-major, `ld` elements between rows and
+ *     `image_stride` elements between images of a batch;
+ *   - device entry points are stream-ordered and asynchronous, allocate
+ *     nothing, and report data-dependent errors through a 2-word device
+ *     status block (see tnrd_status_*);
+ *   - return codes: 0 ok, TNRD_EINVAL (-> ValueError), TNRD_ENONFINITE
+ *     (-> FloatingPointError "non-finite image after stage t"), TNRD_ECUDA
+ *     (-> RuntimeError), TNRD_EUNSUPPORTED (-> NotImplementedError);
+ *     tnrd_last_error() returns the thread's last message.
+ */
+#ifndef TNRD_H
+#define TNRD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define TNRD_OK 0
+#define TNRD_EINVAL 1
+#define TNRD_ENONFINITE 2
+#define TNRD_ECUDA 3
+#define TNRD_EUNSUPPORTED 4
+
+/* tnrd_stage flags */
+#define TNRD_STAGE_FLOOR_INPUT 0x1u  /* u_in := max(u_in, 1e-6) on load (initial_state, diffusion.py:219-224) */
+#define TNRD_STAGE_TOP_HALO 0x2u     /* rows -2r..-1 of u_in are real halo rows (row strip), not mirrored */
+#define TNRD_STAGE_BOTTOM_HALO 0x4u  /* rows H..H+2r-1 of u_in are real halo rows */
+#define TNRD_STAGE_FORCE 0x8u        /* write the diffusion force instead of the prox output */
+#define TNRD_STAGE_CHECK_F 0x10u     /* validate f (finite, >= 0) -> status flags */
+
+/* status block: 2 x uint32 in device memory, reset to 0xFF bytes */
+#define TNRD_STATUS_WORDS 2
+#define TNRD_STATUS_F_NONFINITE 0x1u /* f contained NaN/Inf   (imageops.py:25) */
+#define TNRD_STATUS_F_NEGATIVE 0x2u  /* f contained values < 0 (diffusion.py:231-232) */
+
+typedef struct tnrd_model tnrd_model;
+typedef struct tnrd_plan tnrd_plan;
+
+const char* tnrd_last_error(void);
+const char* tnrd_version(void);
+
+/* Upload one model.  kernels: T*nk*m*m (float64, the reference's true-
+ * convolution kernels k_i); weights: T*nk*M; lam: T (lambda = exp(beta));
+ * centres mu_j = mu0 + j*delta (RbfGrid.centers, influence.py:29-31);
+ * gamma = RbfGrid.gamma (influence.py:33-37).  The handle is immutable after
+ * creation and may be shared between threads/streams. */
+int tnrd_model_create(int m, int nk, int T, int M, const double* kernels,
+                      const double* weights, double mu0, double delta,
+                      double gamma, const double* lam, int device,
+                      tnrd_model** out);
+int tnrd_model_destroy(tnrd_model* model);
+/* m, nk, T, M, rbf path (1 = windowed Horner, 0 = direct all-centre sum) */
+int tnrd_model_info(const tnrd_model* model, int* m, int* nk, int* T, int* M,
+                    int* fast_rbf);
+
+/* Reset a device status block (stream-ordered memset). */
+int tnrd_status_reset(uint32_t* d_status, void* stream);
+/* Decode a HOST copy of the status block: returns TNRD_OK, TNRD_EINVAL (bad
+ * f) or TNRD_ENONFINITE with *bad_stage set; also sets the last error. */
+int tnrd_status_decode(const uint32_t* h_status, int* bad_stage);
+
+/* One stage t of the model: u_out = prox(u_in - force(u_in), f, lam_t)
+ * (or the force with TNRD_STAGE_FORCE).  u_in/f/u_out: device pointers, may
+ * not alias.  For strips, u_in must be addressable 2r rows above row 0 /
+ * below row H-1 on the halo edges. */
+int tnrd_stage(const tnrd_model* model, int t, const float* u_in,
+               const float* f, float* u_out, int batch, int H, int W,
+               int64_t ld, int64_t image_stride, uint32_t flags,
+               uint32_t* d_status, void* stream);
+
+/* All T stages, ping-ponging between u_out and work (same shape), the
+ * final stage landing in u_out.  Stage 0 reads f as u_0 with the 1e-6 floor
+ * (initial_state) and validates f into the status block. */
+int tnrd_despeckle(const tnrd_model* model, const float* f, float* u_out,
+                   float* work, int batch, int H, int W, int64_t ld,
+                   int64_t image_stride, uint32_t* d_status, void* stream);
+
+/* Plans own device buffers, a status block, pinned staging and a stream for
+ * one (batch, H, W) shape; use one plan per host thread. */
+int tnrd_plan_create(const tnrd_model* model, int batch, int H, int W,
+                     tnrd_plan** out);
+int tnrd_plan_destroy(tnrd_plan* plan);
+/* Full despeckle from/to HOST buffers (batch*H*W fp32, dense): H2D, all T
+ * stages, D2H, synchronise, decode status.  Host buffers may be pageable or
+ * pinned. */
+int tnrd_plan_despeckle_host(tnrd_plan* plan, const float* f_host,
+                             float* u_host);
+/* Device-resident variant on the plan's stream (no sync, no status check). */
+int tnrd_plan_despeckle_device(tnrd_plan* plan, const float* f_dev,
+                               float* u_dev);
+/* Synchronise the plan's stream and decode its status block. */
+int tnrd_plan_check(tnrd_plan* plan, int* bad_stage);
+void* tnrd_plan_stream(tnrd_plan* plan);
+/* Device buffers owned by the plan: f (input) and u (output). */
+float* tnrd_plan_f_device(tnrd_plan* plan);
+float* tnrd_plan_u_device(tnrd_plan* plan);
+
+/* Same-size true convolution with half-sample mirror padding (conv2d,
+ * imageops.py:53-72); k: m*m float64 host array, m odd, m <= 15. */
+int tnrd_conv2d(const float* img, float* out, int H, int W, int64_t ld,
+                const double* k, int m, void* stream);
+/* Closed-form I-divergence prox (prox_idiv, speckle.py:111-121). */
+int tnrd_prox_idiv(const float* u_tilde, const float* f, float* out,
+                   int64_t n, double lam, void* stream);
+
+/* Number of kernel launches issued by this library (process-wide) since
+ * the last reset (instrumentation for bench.py's gpu_launches). */
+uint64_t tnrd_launch_count(void);
+void tnrd_launch_count_reset(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TNRD_H */

@@ -1,0 +1,125 @@
+"""ctypes binding of the C ABI in include/tnrd.h (libtnrd.so, built in-tree).
+
+There is no CPU fallback: if the CUDA library is missing or no GPU is
+visible, every compute entry point raises.  Symbol-level loading works
+without a GPU (tests check the exports on CPU).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtnrd.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "tnrd.h")
+
+TNRD_OK = 0
+TNRD_EINVAL = 1
+TNRD_ENONFINITE = 2
+TNRD_ECUDA = 3
+TNRD_EUNSUPPORTED = 4
+
+STAGE_FLOOR_INPUT = 0x1
+STAGE_TOP_HALO = 0x2
+STAGE_BOTTOM_HALO = 0x4
+STAGE_FORCE = 0x8
+STAGE_CHECK_F = 0x10
+
+STATUS_WORDS = 2
+
+_c_int = ctypes.c_int
+_c_i64 = ctypes.c_int64
+_c_u32 = ctypes.c_uint32
+_c_dbl = ctypes.c_double
+_vp = ctypes.c_void_p
+_dp = ctypes.POINTER(ctypes.c_double)
+
+# name -> (restype, argtypes); the test suite checks this table against the
+# declarations in include/tnrd.h.
+SIGNATURES = {
+    "tnrd_last_error": (ctypes.c_char_p, []),
+    "tnrd_version": (ctypes.c_char_p, []),
+    "tnrd_model_create": (_c_int, [_c_int, _c_int, _c_int, _c_int, _dp, _dp,
+                                   _c_dbl, _c_dbl, _c_dbl, _dp, _c_int,
+                                   ctypes.POINTER(_vp)]),
+    "tnrd_model_destroy": (_c_int, [_vp]),
+    "tnrd_model_info": (_c_int, [_vp] + [ctypes.POINTER(_c_int)] * 5),
+    "tnrd_status_reset": (_c_int, [_vp, _vp]),
+    "tnrd_status_decode": (_c_int, [ctypes.POINTER(_c_u32),
+                                    ctypes.POINTER(_c_int)]),
+    "tnrd_stage": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _c_int, _c_int,
+                            _c_int, _c_i64, _c_i64, _c_u32, _vp, _vp]),
+    "tnrd_despeckle": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int,
+                                _c_i64, _c_i64, _vp, _vp]),
+    "tnrd_plan_create": (_c_int, [_vp, _c_int, _c_int, _c_int,
+                                  ctypes.POINTER(_vp)]),
+    "tnrd_plan_destroy": (_c_int, [_vp]),
+    "tnrd_plan_despeckle_host": (_c_int, [_vp, _vp, _vp]),
+    "tnrd_plan_despeckle_device": (_c_int, [_vp, _vp, _vp]),
+    "tnrd_plan_check": (_c_int, [_vp, ctypes.POINTER(_c_int)]),
+    "tnrd_plan_stream": (_vp, [_vp]),
+    "tnrd_plan_f_device": (_vp, [_vp]),
+    "tnrd_plan_u_device": (_vp, [_vp]),
+    "tnrd_conv2d": (_c_int, [_vp, _vp, _c_int, _c_int, _c_i64, _dp, _c_int,
+                             _vp]),
+    "tnrd_prox_idiv": (_c_int, [_vp, _vp, _vp, _c_i64, _c_dbl, _vp]),
+    "tnrd_launch_count": (ctypes.c_uint64, []),
+    "tnrd_launch_count_reset": (None, []),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load():
+    """Load libtnrd.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"CUDA extension not built: {LIB_PATH} is missing "
+                "(run `python -c 'import __graft_entry__ as g; g.build()'`); "
+                "there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    msg = load().tnrd_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int) -> None:
+    """Map a C ABI return code onto the reference's exception types."""
+    if rc == TNRD_OK:
+        return
+    msg = last_error()
+    if rc == TNRD_EINVAL:
+        raise ValueError(msg)
+    if rc == TNRD_ENONFINITE:
+        raise FloatingPointError(msg)
+    if rc == TNRD_EUNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise RuntimeError(msg or f"tnrd error {rc}")
+
+
+def dptr(a) -> _dp:
+    return a.ctypes.data_as(_dp)
+
+
+def launch_count() -> int:
+    return int(load().tnrd_launch_count())
+
+
+def launch_count_reset() -> None:
+    load().tnrd_launch_count_reset()

@@ -1,0 +1,496 @@
+// tnrd_capi.cu -- C ABI (include/tnrd.h) over the fused sm_100a stage kernel.
+//
+// The Python drop-in (paper_1702_07482_b200) binds these symbols with ctypes;
+// nothing here depends on torch.  Host-side parameter preparation follows
+// the reference in float64 (kernels k_i = coeffs @ basis.T are computed by
+// the caller exactly as diffusion.py:76-77 does; this file only casts them
+// and builds the RBF tables), then everything is uploaded once per model.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tnrd.h"
+#include "tnrd_stage.cuh"
+
+using namespace tnrd;
+
+// ----------------------------------------------------------------- errors
+
+static thread_local std::string g_err;
+static std::atomic<uint64_t> g_launches{0};
+
+static int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                              \
+    do {                                                                            \
+        cudaError_t e_ = (expr);                                                    \
+        if (e_ != cudaSuccess)                                                      \
+            return fail(TNRD_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+extern "C" const char* tnrd_last_error(void) { return g_err.c_str(); }
+extern "C" const char* tnrd_version(void) { return "tnrd-b200 0.1.0 sm_100a"; }
+extern "C" uint64_t tnrd_launch_count(void) { return g_launches.load(); }
+extern "C" void tnrd_launch_count_reset(void) { g_launches.store(0); }
+
+// ----------------------------------------------------------------- model
+
+struct tnrd_model {
+    int m = 0, nk = 0, nk_pad = 0, T = 0, M = 0;
+    int device = 0;
+    bool fast = false;
+    int kp = 0;          // floats per filter in taps
+    int tab_stride = 0;  // floats per filter in tab
+    double mu0 = 0, delta = 0, gamma = 0;
+    std::vector<double> lam;
+    float* d_taps = nullptr;  // T * nk_pad * kp
+    float* d_tab = nullptr;   // T * nk_pad * tab_stride
+};
+
+static bool finite_all(const double* p, size_t n) {
+    for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(p[i])) return false;
+    return true;
+}
+
+extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kernels,
+                                 const double* weights, double mu0, double delta,
+                                 double gamma, const double* lam, int device,
+                                 tnrd_model** out) {
+    if (!out) return fail(TNRD_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (m < 1 || m % 2 != 1) return fail(TNRD_EINVAL, "filter size must be odd, got %d", m);
+    if (m != 3 && m != 5 && m != 7 && m != 9)
+        return fail(TNRD_EUNSUPPORTED, "fused stage kernel is built for m in {3,5,7,9}, got %d", m);
+    if (nk < 1) return fail(TNRD_EINVAL, "need at least one filter");
+    if (T < 1) return fail(TNRD_EINVAL, "model needs at least one stage");
+    if (M < 2) return fail(TNRD_EINVAL, "need at least 2 RBF centers");
+    if (!kernels || !weights || !lam) return fail(TNRD_EINVAL, "NULL parameter array");
+    if (!(delta > 0) || !(gamma > 0) || !std::isfinite(mu0))
+        return fail(TNRD_EINVAL, "invalid RBF grid (delta=%g gamma=%g)", delta, gamma);
+    if (!finite_all(kernels, (size_t)T * nk * m * m) || !finite_all(weights, (size_t)T * nk * M))
+        return fail(TNRD_EINVAL, "model parameters contain non-finite values");
+    for (int t = 0; t < T; ++t)
+        if (!(lam[t] > 0) || !std::isfinite(lam[t]))
+            return fail(TNRD_EINVAL, "lambda must be positive, got %g", lam[t]);
+
+    auto* md = new tnrd_model();
+    md->m = m; md->nk = nk; md->T = T; md->M = M; md->device = device;
+    md->nk_pad = round_up(nk, kF);
+    md->mu0 = mu0; md->delta = delta; md->gamma = gamma;
+    md->lam.assign(lam, lam + T);
+    md->kp = round_up(m * m, 4);
+    // windowed Horner RBF is exact (to the truncation bound in DESIGN.md)
+    // when the Gaussians are no wider than the centre spacing and not so
+    // narrow that the window's power series leaves fp32 range.
+    const double rho = delta / gamma;
+    md->fast = rho >= 1.0 - 1e-9 && rho <= 2.0;
+    if (md->fast) {
+        const int ng = (M + kPadL) / 4 + 1;
+        md->tab_stride = ng * kWin;
+    } else {
+        md->tab_stride = round_up(M, 4);
+    }
+
+    const size_t ntap = (size_t)T * md->nk_pad * md->kp;
+    const size_t ntab = (size_t)T * md->nk_pad * md->tab_stride;
+    std::vector<float> taps(ntap, 0.0f), tab(ntab, 0.0f);
+    for (int t = 0; t < T; ++t) {
+        for (int i = 0; i < nk; ++i) {
+            const double* k = kernels + ((size_t)t * nk + i) * m * m;
+            float* dst = taps.data() + ((size_t)t * md->nk_pad + i) * md->kp;
+            for (int j = 0; j < m * m; ++j) dst[j] = (float)k[j];
+            const double* w = weights + ((size_t)t * nk + i) * M;
+            float* tb = tab.data() + ((size_t)t * md->nk_pad + i) * md->tab_stride;
+            if (md->fast) {
+                // A[g][k'] = w_{4g - P + k'} * exp(-(k'-8)^2 delta^2 / (2 gamma^2))
+                const int ng = md->tab_stride / kWin;
+                for (int g = 0; g < ng; ++g)
+                    for (int kq = 0; kq < kWin; ++kq) {
+                        const int j = 4 * g - kPadL + kq;
+                        const double wj = (j >= 0 && j < M) ? w[j] : 0.0;
+                        const double e = std::exp(-(double)((kq - 8) * (kq - 8)) * delta * delta /
+                                                  (2.0 * gamma * gamma));
+                        tb[g * kWin + kq] = (float)(wj * e);
+                    }
+            } else {
+                for (int j = 0; j < M; ++j) tb[j] = (float)w[j];
+            }
+        }
+    }
+    {
+        DeviceGuard dg(device);
+        cudaError_t e1 = cudaMalloc(&md->d_taps, ntap * sizeof(float));
+        cudaError_t e2 = cudaMalloc(&md->d_tab, ntab * sizeof(float));
+        if (e1 != cudaSuccess || e2 != cudaSuccess) {
+            cudaFree(md->d_taps); cudaFree(md->d_tab);
+            delete md;
+            return fail(TNRD_ECUDA, "cudaMalloc of model parameters failed: %s",
+                        cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+        }
+        cudaError_t e3 = cudaMemcpy(md->d_taps, taps.data(), ntap * sizeof(float), cudaMemcpyHostToDevice);
+        cudaError_t e4 = cudaMemcpy(md->d_tab, tab.data(), ntab * sizeof(float), cudaMemcpyHostToDevice);
+        if (e3 != cudaSuccess || e4 != cudaSuccess) {
+            cudaFree(md->d_taps); cudaFree(md->d_tab);
+            delete md;
+            return fail(TNRD_ECUDA, "parameter upload failed: %s",
+                        cudaGetErrorString(e3 != cudaSuccess ? e3 : e4));
+        }
+    }
+    *out = md;
+    return TNRD_OK;
+}
+
+extern "C" int tnrd_model_destroy(tnrd_model* md) {
+    if (!md) return TNRD_OK;
+    {
+        DeviceGuard dg(md->device);
+        cudaFree(md->d_taps);
+        cudaFree(md->d_tab);
+    }
+    delete md;
+    return TNRD_OK;
+}
+
+extern "C" int tnrd_model_info(const tnrd_model* md, int* m, int* nk, int* T, int* M, int* fast) {
+    if (!md) return fail(TNRD_EINVAL, "model is NULL");
+    if (m) *m = md->m;
+    if (nk) *nk = md->nk;
+    if (T) *T = md->T;
+    if (M) *M = md->M;
+    if (fast) *fast = md->fast ? 1 : 0;
+    return TNRD_OK;
+}
+
+// ----------------------------------------------------------------- status
+
+extern "C" int tnrd_status_reset(uint32_t* d_status, void* stream) {
+    if (!d_status) return fail(TNRD_EINVAL, "status is NULL");
+    CUDA_TRY(cudaMemsetAsync(d_status, 0xFF, TNRD_STATUS_WORDS * sizeof(uint32_t),
+                             (cudaStream_t)stream));
+    return TNRD_OK;
+}
+
+extern "C" int tnrd_status_decode(const uint32_t* h, int* bad_stage) {
+    if (bad_stage) *bad_stage = -1;
+    const uint32_t fflags = ~h[1];
+    if (fflags & TNRD_STATUS_F_NONFINITE) return fail(TNRD_EINVAL, "f contains non-finite values");
+    if (fflags & TNRD_STATUS_F_NEGATIVE) return fail(TNRD_EINVAL, "observation must be nonnegative");
+    if (h[0] != 0xFFFFFFFFu) {
+        if (bad_stage) *bad_stage = (int)h[0];
+        return fail(TNRD_ENONFINITE, "non-finite image after stage %d", (int)h[0]);
+    }
+    return TNRD_OK;
+}
+
+// ----------------------------------------------------------------- stage launch
+
+template <int MS, bool FAST>
+struct StageKernel {
+    // tile choice per filter size
+    static constexpr int TH = 32, TW = 32, RF = 2, RB = 2, NT = 128;
+    using C = StageCfg<MS, TH, TW, RF, RB, NT>;
+
+    static int launch(const StageArgs& a, int batch, cudaStream_t s) {
+        static std::mutex mu;
+        static uint64_t attr_set = 0;  // per-device bitmask
+        const size_t smem = C::smem_bytes(a.tab_stride);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        auto kern = stage_kernel<MS, TH, TW, RF, RB, NT, FAST>;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (!(attr_set & (1ull << (dev & 63)))) {
+                CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              160 * 1024));
+                attr_set |= 1ull << (dev & 63);
+            }
+        }
+        dim3 grid((a.W + TW - 1) / TW, (a.H + TH - 1) / TH, batch);
+        kern<<<grid, NT, smem, s>>>(a);
+        CUDA_TRY(cudaGetLastError());
+        g_launches.fetch_add(1);
+        return TNRD_OK;
+    }
+};
+
+template <bool FAST>
+static int dispatch_m(int m, const StageArgs& a, int batch, cudaStream_t s) {
+    switch (m) {
+        case 3: return StageKernel<3, FAST>::launch(a, batch, s);
+        case 5: return StageKernel<5, FAST>::launch(a, batch, s);
+        case 7: return StageKernel<7, FAST>::launch(a, batch, s);
+        case 9: return StageKernel<9, FAST>::launch(a, batch, s);
+        default: return fail(TNRD_EUNSUPPORTED, "unsupported filter size %d", m);
+    }
+}
+
+static int check_shape(const tnrd_model* md, int batch, int H, int W, int64_t ld,
+                       int64_t image_stride) {
+    if (batch < 1 || batch > 65535) return fail(TNRD_EINVAL, "batch must be in [1, 65535], got %d", batch);
+    if (H < 1 || W < 1) return fail(TNRD_EINVAL, "image must have at least one pixel");
+    if (md->m > 2 * std::min(H, W) + 1)
+        return fail(TNRD_EINVAL, "kernel size %d degenerate for image of shape (%d, %d)", md->m, H, W);
+    if (ld < W) return fail(TNRD_EINVAL, "row stride %lld < width %d", (long long)ld, W);
+    if (batch > 1 && image_stride < ld * H)
+        return fail(TNRD_EINVAL, "image stride %lld too small", (long long)image_stride);
+    return TNRD_OK;
+}
+
+static int launch_stage(const tnrd_model* md, int t, const float* u_in, const float* f,
+                        float* u_out, int batch, int H, int W, int64_t ld, int64_t image_stride,
+                        uint32_t flags, uint32_t* d_status, cudaStream_t s) {
+    StageArgs a;
+    a.u_in = u_in; a.f = f; a.u_out = u_out;
+    a.taps = md->d_taps + (size_t)t * md->nk_pad * md->kp;
+    a.tab = md->d_tab + (size_t)t * md->nk_pad * md->tab_stride;
+    a.ld = ld; a.img_stride = image_stride;
+    a.H = H; a.W = W;
+    a.ngroups = md->nk_pad / kF;
+    a.tab_stride = md->tab_stride;
+    const double lam = md->lam[t];
+    const double aa = 1.0 + 2.0 * lam;
+    a.lam4 = (float)(4.0 * lam);
+    a.c8 = (float)(8.0 * aa * lam);
+    a.inv2a = (float)(1.0 / (2.0 * aa));
+    const double L2E = 1.4426950408889634;
+    a.zlo = (float)(md->mu0 - 7.0 * md->delta);
+    a.zhi = (float)(md->mu0 + (md->M - 1 + 7) * md->delta);
+    a.inv_delta = (float)(1.0 / md->delta);
+    a.t_off = (float)(-md->mu0 / md->delta);
+    a.z_off = (float)(-md->mu0);
+    a.delta = (float)md->delta;
+    a.cq = (float)(md->delta * L2E / (md->gamma * md->gamma));
+    a.cE = (float)(-L2E / (2.0 * md->gamma * md->gamma));
+    a.mu0 = (float)md->mu0;
+    a.M = md->M;
+    a.flags = flags;
+    a.stage = t;
+    a.status = d_status;
+    return md->fast ? dispatch_m<true>(md->m, a, batch, s) : dispatch_m<false>(md->m, a, batch, s);
+}
+
+extern "C" int tnrd_stage(const tnrd_model* md, int t, const float* u_in, const float* f,
+                          float* u_out, int batch, int H, int W, int64_t ld, int64_t image_stride,
+                          uint32_t flags, uint32_t* d_status, void* stream) {
+    if (!md) return fail(TNRD_EINVAL, "model is NULL");
+    if (t < 0 || t >= md->T) return fail(TNRD_EINVAL, "stage %d out of range [0, %d)", t, md->T);
+    if (!u_in || !f || !u_out || !d_status) return fail(TNRD_EINVAL, "NULL buffer");
+    if (u_in == u_out) return fail(TNRD_EINVAL, "u_in and u_out must not alias");
+    int rc = check_shape(md, batch, H, W, ld, image_stride);
+    if (rc) return rc;
+    DeviceGuard dg(md->device);
+    return launch_stage(md, t, u_in, f, u_out, batch, H, W, ld, image_stride, flags, d_status,
+                        (cudaStream_t)stream);
+}
+
+extern "C" int tnrd_despeckle(const tnrd_model* md, const float* f, float* u_out, float* work,
+                              int batch, int H, int W, int64_t ld, int64_t image_stride,
+                              uint32_t* d_status, void* stream) {
+    if (!md) return fail(TNRD_EINVAL, "model is NULL");
+    if (!f || !u_out || !d_status || (md->T > 1 && !work)) return fail(TNRD_EINVAL, "NULL buffer");
+    if (f == u_out || f == work || u_out == work) return fail(TNRD_EINVAL, "buffers must not alias");
+    int rc = check_shape(md, batch, H, W, ld, image_stride);
+    if (rc) return rc;
+    DeviceGuard dg(md->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const float* cur = f;
+    for (int t = 0; t < md->T; ++t) {
+        float* dst = ((md->T - 1 - t) % 2 == 0) ? u_out : work;
+        const uint32_t fl = t == 0 ? (TNRD_STAGE_FLOOR_INPUT | TNRD_STAGE_CHECK_F) : 0u;
+        rc = launch_stage(md, t, cur, f, dst, batch, H, W, ld, image_stride, fl, d_status, s);
+        if (rc) return rc;
+        cur = dst;
+    }
+    return TNRD_OK;
+}
+
+// ----------------------------------------------------------------- plans
+
+struct tnrd_plan {
+    const tnrd_model* md = nullptr;
+    int batch = 0, H = 0, W = 0;
+    cudaStream_t stream = nullptr;
+    float *d_f = nullptr, *d_u = nullptr, *d_work = nullptr;
+    uint32_t* d_status = nullptr;
+    uint32_t* h_status = nullptr;  // pinned
+};
+
+extern "C" int tnrd_plan_destroy(tnrd_plan* p) {
+    if (!p) return TNRD_OK;
+    {
+        DeviceGuard dg(p->md->device);
+        if (p->stream) cudaStreamSynchronize(p->stream);
+        cudaFree(p->d_f); cudaFree(p->d_u); cudaFree(p->d_work); cudaFree(p->d_status);
+        if (p->h_status) cudaFreeHost(p->h_status);
+        if (p->stream) cudaStreamDestroy(p->stream);
+    }
+    delete p;
+    return TNRD_OK;
+}
+
+extern "C" int tnrd_plan_create(const tnrd_model* md, int batch, int H, int W, tnrd_plan** out) {
+    if (!out) return fail(TNRD_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!md) return fail(TNRD_EINVAL, "model is NULL");
+    int rc = check_shape(md, batch, H, W, W, (int64_t)W * H);
+    if (rc) return rc;
+    DeviceGuard dg(md->device);
+    auto* p = new tnrd_plan();
+    p->md = md; p->batch = batch; p->H = H; p->W = W;
+    const size_t n = (size_t)batch * H * W;
+    cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_f, n * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_u, n * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_work, n * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_status, TNRD_STATUS_WORDS * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMallocHost(&p->h_status, TNRD_STATUS_WORDS * sizeof(uint32_t));
+    if (e != cudaSuccess) {
+        tnrd_plan_destroy(p);
+        return fail(TNRD_ECUDA, "plan allocation failed: %s", cudaGetErrorString(e));
+    }
+    *out = p;
+    return TNRD_OK;
+}
+
+static int plan_run(tnrd_plan* p, const float* f_dev, float* u_dev) {
+    int rc = tnrd_status_reset(p->d_status, p->stream);
+    if (rc) return rc;
+    return tnrd_despeckle(p->md, f_dev, u_dev, p->d_work, p->batch, p->H, p->W, p->W,
+                          (int64_t)p->W * p->H, p->d_status, p->stream);
+}
+
+extern "C" int tnrd_plan_despeckle_device(tnrd_plan* p, const float* f_dev, float* u_dev) {
+    if (!p) return fail(TNRD_EINVAL, "plan is NULL");
+    DeviceGuard dg(p->md->device);
+    return plan_run(p, f_dev ? f_dev : p->d_f, u_dev ? u_dev : p->d_u);
+}
+
+extern "C" int tnrd_plan_check(tnrd_plan* p, int* bad_stage) {
+    if (!p) return fail(TNRD_EINVAL, "plan is NULL");
+    DeviceGuard dg(p->md->device);
+    CUDA_TRY(cudaMemcpyAsync(p->h_status, p->d_status, TNRD_STATUS_WORDS * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    return tnrd_status_decode(p->h_status, bad_stage);
+}
+
+extern "C" int tnrd_plan_despeckle_host(tnrd_plan* p, const float* f_host, float* u_host) {
+    if (!p) return fail(TNRD_EINVAL, "plan is NULL");
+    if (!f_host || !u_host) return fail(TNRD_EINVAL, "NULL host buffer");
+    DeviceGuard dg(p->md->device);
+    const size_t bytes = (size_t)p->batch * p->H * p->W * sizeof(float);
+    CUDA_TRY(cudaMemcpyAsync(p->d_f, f_host, bytes, cudaMemcpyHostToDevice, p->stream));
+    int rc = plan_run(p, p->d_f, p->d_u);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(u_host, p->d_u, bytes, cudaMemcpyDeviceToHost, p->stream));
+    int bad = -1;
+    return tnrd_plan_check(p, &bad);
+}
+
+extern "C" void* tnrd_plan_stream(tnrd_plan* p) { return p ? (void*)p->stream : nullptr; }
+extern "C" float* tnrd_plan_f_device(tnrd_plan* p) { return p ? p->d_f : nullptr; }
+extern "C" float* tnrd_plan_u_device(tnrd_plan* p) { return p ? p->d_u : nullptr; }
+
+// ----------------------------------------------------------------- conv2d / prox
+
+struct ConvTaps {
+    float k[225];
+};
+
+// imageops.py:53-72: out[y,x] = sum_{a,b} k[a,b] img[mir(y+r-a), mir(x+r-b)]
+__global__ void conv2d_kernel(const float* __restrict__ img, float* __restrict__ out, int H, int W,
+                              int64_t ld, int m, const ConvTaps taps) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= W || y >= H) return;
+    const int r = m / 2;
+    float s = 0.0f;
+    for (int a = 0; a < m; ++a) {
+        int yy = y + r - a;
+        yy = yy < 0 ? -1 - yy : (yy >= H ? 2 * H - 1 - yy : yy);
+        for (int b = 0; b < m; ++b) {
+            int xx = x + r - b;
+            xx = xx < 0 ? -1 - xx : (xx >= W ? 2 * W - 1 - xx : xx);
+            s = fmaf(taps.k[a * m + b], __ldg(img + (int64_t)yy * ld + xx), s);
+        }
+    }
+    out[(int64_t)y * ld + x] = s;
+}
+
+extern "C" int tnrd_conv2d(const float* img, float* out, int H, int W, int64_t ld, const double* k,
+                           int m, void* stream) {
+    if (!img || !out || !k) return fail(TNRD_EINVAL, "NULL buffer");
+    if (m < 1 || m % 2 != 1) return fail(TNRD_EINVAL, "kernel side must be odd, got %d", m);
+    if (m > 15) return fail(TNRD_EUNSUPPORTED, "conv2d supports m <= 15, got %d", m);
+    if (H < 1 || W < 1) return fail(TNRD_EINVAL, "image must have at least one pixel");
+    if (m > 2 * std::min(H, W) + 1)
+        return fail(TNRD_EINVAL, "kernel size %d degenerate for image of shape (%d, %d)", m, H, W);
+    if (ld < W) return fail(TNRD_EINVAL, "row stride too small");
+    ConvTaps taps;
+    for (int i = 0; i < m * m; ++i) {
+        if (!std::isfinite(k[i])) return fail(TNRD_EINVAL, "kernel contains non-finite values");
+        taps.k[i] = (float)k[i];
+    }
+    dim3 blk(32, 8), grid((W + 31) / 32, (H + 7) / 8);
+    conv2d_kernel<<<grid, blk, 0, (cudaStream_t)stream>>>(img, out, H, W, ld, m, taps);
+    CUDA_TRY(cudaGetLastError());
+    g_launches.fetch_add(1);
+    return TNRD_OK;
+}
+
+// speckle.py:111-121 (cancellation-free for u~ < 0)
+__global__ void prox_kernel(const float* __restrict__ ut, const float* __restrict__ f,
+                            float* __restrict__ out, int64_t n, float lam4, float c8, float inv2a) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float u = ut[i];
+        const float ff = fmaxf(f[i], kFFloor);
+        const float fl2 = ff * ff;
+        const float root = sqrtf(fmaf(u, u, c8 * fl2));
+        out[i] = u >= 0.0f ? (u + root) * inv2a : (lam4 * fl2) / (root - u);
+    }
+}
+
+extern "C" int tnrd_prox_idiv(const float* ut, const float* f, float* out, int64_t n, double lam,
+                              void* stream) {
+    if (!(lam > 0)) return fail(TNRD_EINVAL, "lambda must be positive, got %g", lam);
+    if (n <= 0) return TNRD_OK;
+    if (!ut || !f || !out) return fail(TNRD_EINVAL, "NULL buffer");
+    const double a = 1.0 + 2.0 * lam;
+    const int threads = 256;
+    const int64_t blocks = std::min<int64_t>((n + threads - 1) / threads, 148 * 16);
+    prox_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
+        ut, f, out, n, (float)(4.0 * lam), (float)(8.0 * a * lam), (float)(1.0 / (2.0 * a)));
+    CUDA_TRY(cudaGetLastError());
+    g_launches.fetch_add(1);
+    return TNRD_OK;
+}

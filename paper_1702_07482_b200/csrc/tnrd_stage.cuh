@@ -1,0 +1,405 @@
+// tnrd_stage.cuh -- fused TNRD diffusion stage for sm_100a.
+//
+// One launch = one stage of diffusion_step (reference diffusion.py:184-194)
+// over a batch of images:
+//
+//   z_i   = conv2d(u, k_i)                 imageops.py:53-72 (mirror padded)
+//   phi_i = sum_j w_ij exp(-(z_i-mu_j)^2/(2 gamma^2))   influence.py:40-45
+//   force = sum_i conv2d(phi_i, rot180(k_i))   diffusion.py:178-180 (phi is
+//           mirror padded itself, NOT the exact adjoint)
+//   u'    = prox_idiv(u - force, f, lam)   speckle.py:111-121
+//
+// B200 mapping (see DESIGN.md for the derivation):
+//   * a CTA owns a TH x TW output tile; u is staged in shared memory with a
+//     2r halo, phi for F filters at a time with an r halo;
+//   * filters are processed in groups of F; the group's taps and RBF tables
+//     are prefetched into shared memory with cp.async one group ahead;
+//   * forward pass: each work item = one filter x RF x 4 phi block; the 49
+//     taps live in registers, u rows are read as float4;
+//   * the RBF is evaluated exactly (to < 1e-9 relative to the weights) with
+//     a 16-centre window around z: phi = E(d) * [P+(q) + P-(1/q)], two
+//     Horner chains over a per-filter pre-scaled weight table, 3 ex2 per
+//     response instead of M=63;
+//   * phi halos that fall outside the image are filled by mirroring the
+//     in-image phi values (reference pads phi itself, diffusion.py:180);
+//   * backward pass: each thread owns an RB x 4 output block and keeps the
+//     force in registers across all filter groups;
+//   * epilogue: u~ = u - force, cancellation-free prox, non-finite flag,
+//     f validation (stage 0), store.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tnrd {
+
+constexpr int kF = 4;          // filters per group
+constexpr int kWin = 16;       // RBF window (centres) of the fast path
+constexpr int kPadL = 16;      // table padding (centres) left of mu_0
+constexpr int kHalfWin = 6;    // window must cover j0-6 .. j0+6
+constexpr float kFFloor = 1e-6f;  // speckle.py:21
+
+__host__ __device__ constexpr int round_up(int x, int a) { return (x + a - 1) / a * a; }
+
+struct StageArgs {
+    const float* u_in;
+    const float* f;
+    float* u_out;
+    const float* taps;   // [nk_pad][KP]  reference k_i (row-major a,b)
+    const float* tab;    // [nk_pad][tab_stride] RBF table (fast: Horner A, generic: w)
+    int64_t ld;          // elements between rows
+    int64_t img_stride;  // elements between images
+    int H, W;
+    int ngroups;         // nk_pad / kF
+    int tab_stride;      // floats per filter in tab
+    // prox (speckle.py:111-121): a = 1 + 2 lam
+    float lam4;          // 4 lam
+    float c8;            // 8 a lam
+    float inv2a;         // 1 / (2a)
+    // RBF constants
+    float zlo, zhi;      // z clamp (fast path)
+    float inv_delta;     // 1 / delta
+    float t_off;         // -mu0 / delta
+    float z_off;         // -mu0
+    float delta;
+    float cq;            // delta * log2(e) / gamma^2
+    float cE;            // -log2(e) / (2 gamma^2)
+    float mu0;           // generic path
+    int M;               // generic path: number of centres
+    uint32_t flags;
+    int stage;
+    uint32_t* status;    // [0] first non-finite stage (atomicMin), [1] f flags (atomicAnd ~bit)
+};
+
+__device__ __forceinline__ float ex2f(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// Half-sample symmetric reflection (np.pad mode="symmetric", one fold) and
+// clamp: positions further out than one fold only feed discarded outputs.
+__device__ __forceinline__ int mirror_clamp(int j, int n) {
+    j = j < 0 ? -1 - j : j;
+    j = j >= n ? 2 * n - 1 - j : j;
+    return min(max(j, 0), n - 1);
+}
+
+// phi(z) with the windowed two-chain Horner form (fast path, gamma <= delta).
+//   window start (table index) ps = (j0 + kPadL - kHalfWin) & ~3, middle
+//   centre c = ps - kPadL + 8, d = z - mu_c, q = exp(delta d / gamma^2),
+//   E = exp(-d^2 / (2 gamma^2)), A[k'] = w_{c-8+k'} exp(-(k'-8)^2 delta^2 / (2 gamma^2)):
+//   phi = E * (sum_{k'>=8} A[k'] q^(k'-8) + sum_{k'<8} A[k'] (1/q)^(8-k'))
+__device__ __forceinline__ float rbf_fast(float z, const float* __restrict__ tabf,
+                                          const StageArgs& p) {
+    z = fminf(fmaxf(z, p.zlo), p.zhi);
+    const float t = fmaf(z, p.inv_delta, p.t_off);
+    const int j0 = __float_as_int(t + 12582912.0f) - 0x4B400000;  // rint(t)
+    const int ps = (j0 + (kPadL - kHalfWin)) & ~3;
+    const float fc = __int_as_float(ps + (0x4B400000 + 8 - kPadL)) - 12582912.0f;
+    const float d = fmaf(-p.delta, fc, z + p.z_off);
+    const float x = d * p.cq;
+    const float q = ex2f(x);
+    const float qi = ex2f(-x);
+    const float E = ex2f(d * d * p.cE);
+    const float4* A = reinterpret_cast<const float4*>(tabf + ps * 4);
+    const float4 a0 = A[0], a1 = A[1], a2 = A[2], a3 = A[3];
+    float hp = fmaf(a3.w, q, a3.z);
+    hp = fmaf(hp, q, a3.y);
+    hp = fmaf(hp, q, a3.x);
+    hp = fmaf(hp, q, a2.w);
+    hp = fmaf(hp, q, a2.z);
+    hp = fmaf(hp, q, a2.y);
+    hp = fmaf(hp, q, a2.x);
+    float hm = fmaf(a0.x, qi, a0.y);
+    hm = fmaf(hm, qi, a0.z);
+    hm = fmaf(hm, qi, a0.w);
+    hm = fmaf(hm, qi, a1.x);
+    hm = fmaf(hm, qi, a1.y);
+    hm = fmaf(hm, qi, a1.z);
+    hm = fmaf(hm, qi, a1.w);
+    return E * fmaf(hm, qi, hp);
+}
+
+// phi(z) as the reference writes it: all M centres (generic bandwidths).
+__device__ __forceinline__ float rbf_direct(float z, const float* __restrict__ w,
+                                            const StageArgs& p) {
+    float s = 0.0f;
+    for (int j = 0; j < p.M; ++j) {
+        const float d = z - fmaf((float)j, p.delta, p.mu0);
+        s = fmaf(w[j], ex2f(d * d * p.cE), s);
+    }
+    return s;
+}
+
+template <int MS, int TH, int TW, int RF, int RB, int NT>
+struct StageCfg {
+    static constexpr int R = MS / 2;
+    static constexpr int PH = round_up(TH + 2 * R, RF);  // phi rows computed
+    static constexpr int PW = round_up(TW + 2 * R, 4);   // phi cols computed (stride)
+    static constexpr int UR = PH + 2 * R;                // u rows staged
+    static constexpr int US = PW + round_up(2 * R, 4);   // u row stride
+    static constexpr int NV = (4 + 2 * R + 3) / 4;       // float4 per row segment
+    static constexpr int KK = MS * MS;
+    static constexpr int KP = round_up(KK, 4);
+    static constexpr int NBX = PW / 4;                   // forward blocks per row
+    static constexpr int NBY = PH / RF;
+    static constexpr int FWD_ITEMS = NBX * NBY * kF;
+    static constexpr int OBX = TW / 4;                   // output blocks
+    static constexpr int OBY = TH / RB;
+    static_assert(OBX * OBY == NT, "one output block per thread");
+    static_assert(TW % 4 == 0 && TH % RB == 0, "tile shape");
+    static constexpr int SU = UR * US;
+    static constexpr int SPHI = PH * PW;
+    // shared layout (floats): u | phi[F] | taps[2][F*KP] | tab[2][F*tab_stride]
+    static size_t smem_bytes(int tab_stride) {
+        return sizeof(float) * (size_t)(SU + kF * SPHI + 2 * kF * KP + 2 * kF * tab_stride);
+    }
+};
+
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST>
+__global__ void __launch_bounds__(NT, 4) stage_kernel(const StageArgs p) {
+    using C = StageCfg<MS, TH, TW, RF, RB, NT>;
+    constexpr int R = C::R;
+    extern __shared__ __align__(16) float smem[];
+    float* sU = smem;
+    float* sPhi = sU + C::SU;
+    float* sTap = sPhi + kF * C::SPHI;
+    float* sTab = sTap + 2 * kF * C::KP;
+    const int tabsz = kF * p.tab_stride;
+
+    const int tid = threadIdx.x;
+    const int img = blockIdx.z;
+    const int Y0 = blockIdx.y * TH;
+    const int X0 = blockIdx.x * TW;
+    const float* __restrict__ uin = p.u_in + (int64_t)img * p.img_stride;
+    const float* __restrict__ fin = p.f + (int64_t)img * p.img_stride;
+    float* __restrict__ uout = p.u_out + (int64_t)img * p.img_stride;
+    const bool top_halo = p.flags & 0x2u;
+    const bool bot_halo = p.flags & 0x4u;
+
+    // prefetch group 0 parameters
+    auto prefetch = [&](int g, int buf) {
+        const float* gt = p.taps + (size_t)g * kF * C::KP;
+        float* st = sTap + buf * kF * C::KP;
+        for (int i = tid; i < kF * C::KP / 4; i += NT) cp_async16(st + 4 * i, gt + 4 * i);
+        const float* gb = p.tab + (size_t)g * tabsz;
+        float* sb = sTab + buf * tabsz;
+        for (int i = tid; i < tabsz / 4; i += NT) cp_async16(sb + 4 * i, gb + 4 * i);
+        cp_async_commit();
+    };
+    prefetch(0, 0);
+
+    // ---- stage u tile (2r halo), mirrored at image edges --------------------
+    {
+        const bool floor_in = p.flags & 0x1u;
+        for (int i = tid; i < C::SU; i += NT) {
+            const int uy = i / C::US, ux = i - uy * C::US;
+            int Y = Y0 - 2 * R + uy;
+            int X = mirror_clamp(X0 - 2 * R + ux, p.W);
+            if (Y < 0) Y = top_halo ? max(Y, -2 * R) : mirror_clamp(Y, p.H);
+            else if (Y >= p.H) Y = bot_halo ? min(Y, p.H - 1 + 2 * R) : mirror_clamp(Y, p.H);
+            float v = __ldg(uin + (int64_t)Y * p.ld + X);
+            if (floor_in) v = fmaxf(v, kFFloor);
+            sU[i] = v;
+        }
+    }
+
+    // tile touches a mirrored image edge? (phi halo fix-up needed)
+    const bool fix_l = X0 - R < 0;
+    const bool fix_r = X0 + TW + R > p.W;
+    const bool fix_t = !top_halo && (Y0 - R < 0);
+    const bool fix_b = !bot_halo && (Y0 + TH + R > p.H);
+    const bool need_fix = fix_l || fix_r || fix_t || fix_b;
+
+    const int obx = tid % C::OBX, oby = tid / C::OBX;
+    const int ox0 = obx * 4, oy0 = oby * RB;
+    float force[RB][4];
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) force[r][c] = 0.0f;
+
+    for (int g = 0; g < p.ngroups; ++g) {
+        const int buf = g & 1;
+        cp_async_wait_all();
+        __syncthreads();  // params of group g landed; previous bwd done with sPhi
+        if (g + 1 < p.ngroups) prefetch(g + 1, buf ^ 1);
+        const float* tapg = sTap + buf * kF * C::KP;
+        const float* tabg = sTab + buf * tabsz;
+
+        // ---- forward: z = conv(u, k) on the phi region, phi = rbf(z) --------
+        for (int it = tid; it < C::FWD_ITEMS; it += NT) {
+            const int bx = it % C::NBX;
+            const int rest = it / C::NBX;
+            const int by = rest % C::NBY;
+            const int fi = rest / C::NBY;
+            const int x0 = bx * 4, y0 = by * RF;
+            float k[C::KK];
+            {
+                const float4* t4 = reinterpret_cast<const float4*>(tapg + fi * C::KP);
+#pragma unroll
+                for (int q = 0; q < C::KP / 4; ++q) {
+                    const float4 v = t4[q];
+                    if (4 * q + 0 < C::KK) k[4 * q + 0] = v.x;
+                    if (4 * q + 1 < C::KK) k[4 * q + 1] = v.y;
+                    if (4 * q + 2 < C::KK) k[4 * q + 2] = v.z;
+                    if (4 * q + 3 < C::KK) k[4 * q + 3] = v.w;
+                }
+            }
+            float acc[RF][4];
+#pragma unroll
+            for (int r = 0; r < RF; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
+#pragma unroll
+            for (int rr = 0; rr < RF + 2 * R; ++rr) {
+                float v[4 * C::NV];
+                const float4* src = reinterpret_cast<const float4*>(sU + (y0 + rr) * C::US + x0);
+#pragma unroll
+                for (int q = 0; q < C::NV; ++q) {
+                    const float4 t = src[q];
+                    v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+                }
+#pragma unroll
+                for (int a = 0; a < MS; ++a) {
+                    const int ro = rr - a;
+                    if (ro >= 0 && ro < RF) {
+#pragma unroll
+                        for (int b = 0; b < MS; ++b) {
+                            // true convolution == correlation with rot180(k)
+                            const float kk = k[(MS - 1 - a) * MS + (MS - 1 - b)];
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) acc[ro][c] = fmaf(kk, v[c + b], acc[ro][c]);
+                        }
+                    }
+                }
+            }
+            const float* tabf = tabg + fi * p.tab_stride;
+            float* dst = sPhi + fi * C::SPHI + y0 * C::PW + x0;
+#pragma unroll
+            for (int r = 0; r < RF; ++r) {
+                float4 o;
+                if (FAST) {
+                    o.x = rbf_fast(acc[r][0], tabf, p);
+                    o.y = rbf_fast(acc[r][1], tabf, p);
+                    o.z = rbf_fast(acc[r][2], tabf, p);
+                    o.w = rbf_fast(acc[r][3], tabf, p);
+                } else {
+                    o.x = rbf_direct(acc[r][0], tabf, p);
+                    o.y = rbf_direct(acc[r][1], tabf, p);
+                    o.z = rbf_direct(acc[r][2], tabf, p);
+                    o.w = rbf_direct(acc[r][3], tabf, p);
+                }
+                *reinterpret_cast<float4*>(dst + r * C::PW) = o;
+            }
+        }
+        __syncthreads();
+
+        // ---- phi halo outside the image = mirror of in-image phi -------------
+        if (need_fix) {
+            // phi-region (py, px) <-> image (Y0 - R + py, X0 - R + px)
+            for (int i = tid; i < kF * C::SPHI; i += NT) {
+                const int fi = i / C::SPHI;
+                const int rem = i - fi * C::SPHI;
+                const int py = rem / C::PW, px = rem - py * C::PW;
+                const int Y = Y0 - R + py, X = X0 - R + px;
+                int sy = Y, sx = X;
+                if (X < 0 && X >= -R) sx = -1 - X;
+                else if (X >= p.W && X < p.W + R) sx = 2 * p.W - 1 - X;
+                if (!top_halo && Y < 0 && Y >= -R) sy = -1 - Y;
+                else if (!bot_halo && Y >= p.H && Y < p.H + R) sy = 2 * p.H - 1 - Y;
+                if (sy != Y || sx != X) {
+                    const int spy = sy - (Y0 - R), spx = sx - (X0 - R);
+                    sPhi[fi * C::SPHI + py * C::PW + px] = sPhi[fi * C::SPHI + spy * C::PW + spx];
+                }
+            }
+            __syncthreads();
+        }
+
+        // ---- backward: force += corr(phi_i, k_i) -----------------------------
+#pragma unroll 1
+        for (int fi = 0; fi < kF; ++fi) {
+            float k[C::KK];
+            {
+                const float4* t4 = reinterpret_cast<const float4*>(tapg + fi * C::KP);
+#pragma unroll
+                for (int q = 0; q < C::KP / 4; ++q) {
+                    const float4 v = t4[q];
+                    if (4 * q + 0 < C::KK) k[4 * q + 0] = v.x;
+                    if (4 * q + 1 < C::KK) k[4 * q + 1] = v.y;
+                    if (4 * q + 2 < C::KK) k[4 * q + 2] = v.z;
+                    if (4 * q + 3 < C::KK) k[4 * q + 3] = v.w;
+                }
+            }
+            const float* ph = sPhi + fi * C::SPHI;
+#pragma unroll
+            for (int rr = 0; rr < RB + 2 * R; ++rr) {
+                float v[4 * C::NV];
+                const float4* src = reinterpret_cast<const float4*>(ph + (oy0 + rr) * C::PW + ox0);
+#pragma unroll
+                for (int q = 0; q < C::NV; ++q) {
+                    const float4 t = src[q];
+                    v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+                }
+#pragma unroll
+                for (int a = 0; a < MS; ++a) {
+                    const int ro = rr - a;
+                    if (ro >= 0 && ro < RB) {
+#pragma unroll
+                        for (int b = 0; b < MS; ++b) {
+                            const float kk = k[a * MS + b];
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) force[ro][c] = fmaf(kk, v[c + b], force[ro][c]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+
+    // ---- epilogue: u~ = u - force, prox, checks, store ----------------------
+    const bool out_force = p.flags & 0x8u;
+    const bool check_f = p.flags & 0x10u;
+    bool bad = false;
+    uint32_t fbits = 0;
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+        const int Y = Y0 + oy0 + r;
+        if (Y >= p.H) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int X = X0 + ox0 + c;
+            if (X >= p.W) continue;
+            float res;
+            if (out_force) {
+                res = force[r][c];
+            } else {
+                const float u = sU[(oy0 + r + 2 * R) * C::US + ox0 + c + 2 * R];
+                const float fv = __ldg(fin + (int64_t)Y * p.ld + X);
+                if (check_f) {
+                    if (!isfinite(fv)) fbits |= 0x1u;
+                    else if (fv < 0.0f) fbits |= 0x2u;
+                }
+                const float ff = fmaxf(fv, kFFloor);
+                const float ut = u - force[r][c];
+                const float fl2 = ff * ff;
+                const float root = sqrtf(fmaf(ut, ut, p.c8 * fl2));
+                // (ut + root)/(2a), cancellation-free for ut < 0
+                res = ut >= 0.0f ? (ut + root) * p.inv2a : (p.lam4 * fl2) / (root - ut);
+            }
+            if (!isfinite(res)) bad = true;
+            uout[(int64_t)Y * p.ld + X] = res;
+        }
+    }
+    if (bad) atomicMin(p.status, (uint32_t)p.stage);
+    if (fbits) atomicAnd(p.status + 1, ~fbits);
+}
+
+}  // namespace tnrd

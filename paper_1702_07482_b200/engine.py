@@ -1,0 +1,297 @@
+"""Device-side engine: one uploaded model, stream-ordered launches, plans.
+
+This is the layer between the reference-shaped Python API (diffusion.py)
+and the C ABI (include/tnrd.h).  PyTorch is used only for device memory,
+streams and torch.distributed plumbing; every kernel that touches the data
+is in libtnrd.so.
+"""
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import math
+import threading
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def require_cuda() -> None:
+    if not torch().cuda.is_available():
+        raise RuntimeError("no CUDA device is visible: the TNRD path is GPU-only "
+                           "(there is no CPU fallback)")
+
+
+def _stream_handle(stream=None) -> ctypes.c_void_p:
+    t = torch()
+    s = stream if stream is not None else t.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(tensor) -> ctypes.c_void_p:
+    return ctypes.c_void_p(tensor.data_ptr())
+
+
+def rbf_grid_params(count: int, radius: float, bandwidth=None):
+    """(mu0, delta, gamma) of RbfGrid (influence.py:29-37): centres are
+    np.linspace(-radius, radius, count), gamma defaults to the spacing."""
+    delta = 2.0 * radius / (count - 1)
+    gamma = float(bandwidth) if bandwidth is not None else delta
+    return -float(radius), float(delta), float(gamma)
+
+
+def params_fingerprint(m: int, kernels: np.ndarray, weights: np.ndarray,
+                       lams: np.ndarray, grid: tuple) -> str:
+    h = hashlib.blake2b(digest_size=16)
+    h.update(np.asarray([m], dtype=np.int64).tobytes())
+    for a in (kernels, weights, lams, np.asarray(grid, dtype=np.float64)):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        h.update(np.asarray(a.shape, dtype=np.int64).tobytes())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+class Status:
+    """Device status block (2 x uint32): first non-finite stage, f flags."""
+
+    def __init__(self, device):
+        t = torch()
+        self.buf = t.empty(_lib.STATUS_WORDS, dtype=t.int32, device=device)
+
+    def reset(self, stream=None) -> None:
+        _lib.check(_lib.load().tnrd_status_reset(_ptr(self.buf),
+                                                 _stream_handle(stream)))
+
+    def check(self) -> None:
+        """Synchronise (via the D2H copy) and raise the reference's error."""
+        host = self.buf.cpu().numpy().view(np.uint32).copy()
+        arr = (ctypes.c_uint32 * _lib.STATUS_WORDS)(*host.tolist())
+        bad = ctypes.c_int(-1)
+        _lib.check(_lib.load().tnrd_status_decode(arr, ctypes.byref(bad)))
+
+
+class DeviceModel:
+    """A DiffusionModel uploaded to one GPU (tnrd_model_create).
+
+    kernels: (T, nk, m, m) float64 -- the reference's true-convolution
+    kernels k_i = coeffs @ basis.T (diffusion.py:76-77); weights (T, nk, M);
+    lams (T,) with lambda = exp(beta) (diffusion.py:72-74).
+    """
+
+    def __init__(self, kernels, weights, lams, grid, device=None):
+        require_cuda()
+        t = torch()
+        L = _lib.load()
+        k = np.ascontiguousarray(kernels, dtype=np.float64)
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        lm = np.ascontiguousarray(lams, dtype=np.float64)
+        if k.ndim != 4 or k.shape[2] != k.shape[3]:
+            raise ValueError("kernels must be (T, nk, m, m)")
+        T, nk, m, _ = k.shape
+        if w.ndim != 3 or w.shape[:2] != (T, nk):
+            raise ValueError("weights must be (T, nk, M)")
+        if lm.shape != (T,):
+            raise ValueError("need one lambda per stage")
+        M = w.shape[2]
+        mu0, delta, gamma = grid
+        self.device = t.device("cuda", t.cuda.current_device()
+                               if device is None else int(device))
+        self.m, self.nk, self.T, self.M = m, nk, T, M
+        self.grid = (mu0, delta, gamma)
+        h = ctypes.c_void_p()
+        _lib.check(L.tnrd_model_create(m, nk, T, M, _lib.dptr(k), _lib.dptr(w),
+                                       mu0, delta, gamma, _lib.dptr(lm),
+                                       self.device.index, ctypes.byref(h)))
+        self.handle = h
+        fast = ctypes.c_int(0)
+        _lib.check(L.tnrd_model_info(h, None, None, None, None,
+                                     ctypes.byref(fast)))
+        self.fast_rbf = bool(fast.value)
+        self._plans = {}
+        self._plan_lock = threading.Lock()
+        self._status = {}
+
+    # ---------------------------------------------------------- lifecycle
+    def close(self) -> None:
+        L = _lib._lib
+        if L is None or self.handle is None:
+            return
+        for p in self._plans.values():
+            L.tnrd_plan_destroy(p)
+        self._plans.clear()
+        L.tnrd_model_destroy(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def radius(self) -> int:
+        return self.m // 2
+
+    def status(self) -> Status:
+        key = threading.get_ident()
+        s = self._status.get(key)
+        if s is None:
+            s = self._status[key] = Status(self.device)
+        return s
+
+    # ---------------------------------------------------------- device API
+    def _shape(self, x):
+        if x.dim() == 2:
+            return 1, x.shape[0], x.shape[1]
+        if x.dim() == 3:
+            return x.shape[0], x.shape[1], x.shape[2]
+        raise ValueError(f"expected (H, W) or (B, H, W), got {tuple(x.shape)}")
+
+    def _check_tensor(self, x, name):
+        t = torch()
+        if x.device != self.device:
+            raise ValueError(f"{name} is on {x.device}, model on {self.device}")
+        if x.dtype != t.float32:
+            raise ValueError(f"{name} must be float32")
+        if x.stride(-1) != 1:
+            raise ValueError(f"{name} rows must be contiguous")
+
+    def despeckle(self, f, out=None, work=None, stream=None, check=True):
+        """run_diffusion on device tensors: f (H, W) or (B, H, W) fp32 CUDA.
+        Returns u_T (same shape).  With check=False the status block is left
+        for a later ``status().check()`` (no host synchronisation)."""
+        t = torch()
+        self._check_tensor(f, "f")
+        B, H, W = self._shape(f)
+        if out is None:
+            out = t.empty_like(f, memory_format=t.contiguous_format)
+        if work is None and self.T > 1:
+            work = t.empty_like(out)
+        for name, x in (("out", out), ("work", work)):
+            if x is not None:
+                self._check_tensor(x, name)
+                if x.shape != f.shape or x.stride() != out.stride():
+                    raise ValueError(f"{name} must match f's shape/strides")
+        if f.stride() != out.stride():
+            f = f.contiguous()
+        ld = f.stride(-2)
+        img_stride = f.stride(0) if f.dim() == 3 else ld * H
+        st = self.status()
+        st.reset(stream)
+        _lib.check(_lib.load().tnrd_despeckle(
+            self.handle, _ptr(f), _ptr(out),
+            _ptr(work) if work is not None else None, B, H, W, ld, img_stride,
+            _ptr(st.buf), _stream_handle(stream)))
+        if check:
+            st.check()
+        return out
+
+    def stage(self, t_index: int, u, f, out=None, flags: int = 0,
+              stream=None, status: Status | None = None, rows=None):
+        """One stage on device tensors.  ``rows`` = (row0, H) restricts the
+        stage to rows [row0, row0 + H) of u/f/out (row strips: u must then
+        carry the halo rows around that window when TOP/BOTTOM_HALO is set)."""
+        t = torch()
+        self._check_tensor(u, "u")
+        self._check_tensor(f, "f")
+        if out is None:
+            out = t.empty_like(u)
+        self._check_tensor(out, "out")
+        B, H, W = self._shape(u)
+        if u.stride() != f.stride() or u.stride() != out.stride():
+            raise ValueError("u, f and out must share strides")
+        ld = u.stride(-2)
+        img_stride = u.stride(0) if u.dim() == 3 else ld * H
+        row0 = 0
+        if rows is not None:
+            row0, H = int(rows[0]), int(rows[1])
+        off = row0 * ld * u.element_size()
+        st = status if status is not None else self.status()
+        if status is None:
+            st.reset(stream)
+        _lib.check(_lib.load().tnrd_stage(
+            self.handle, int(t_index), ctypes.c_void_p(u.data_ptr() + off),
+            ctypes.c_void_p(f.data_ptr() + off),
+            ctypes.c_void_p(out.data_ptr() + off), B, H, W, ld, img_stride,
+            int(flags), _ptr(st.buf), _stream_handle(stream)))
+        if status is None:
+            st.check()
+        return out
+
+    # ---------------------------------------------------------- host API
+    def _plan(self, B, H, W):
+        key = (threading.get_ident(), B, H, W)
+        p = self._plans.get(key)
+        if p is None:
+            with self._plan_lock:
+                p = self._plans.get(key)
+                if p is None:
+                    h = ctypes.c_void_p()
+                    _lib.check(_lib.load().tnrd_plan_create(
+                        self.handle, B, H, W, ctypes.byref(h)))
+                    p = self._plans[key] = h
+        return p
+
+    def despeckle_host(self, f: np.ndarray, out: np.ndarray | None = None):
+        """Full despeckle of HOST fp32 arrays through the plan C ABI
+        (tnrd_plan_despeckle_host: H2D, T stages, D2H, status check)."""
+        f = np.ascontiguousarray(f, dtype=np.float32)
+        if f.ndim == 2:
+            B, (H, W) = 1, f.shape
+        elif f.ndim == 3:
+            B, H, W = f.shape
+        else:
+            raise ValueError(f"expected (H, W) or (B, H, W), got {f.shape}")
+        if out is None:
+            out = np.empty_like(f)
+        elif out.shape != f.shape or out.dtype != np.float32 or \
+                not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float32 array like f")
+        p = self._plan(B, H, W)
+        _lib.check(_lib.load().tnrd_plan_despeckle_host(
+            p, f.ctypes.data_as(ctypes.c_void_p),
+            out.ctypes.data_as(ctypes.c_void_p)))
+        return out
+
+
+def model_kernels(model, stages: Sequence | None = None) -> np.ndarray:
+    """(T, nk, m, m) float64 kernels of a DiffusionModel, exactly as the
+    reference builds them (diffusion.py:76-77, 189)."""
+    stages = model.stages if stages is None else stages
+    return np.stack([s.kernels(model.basis, model.filter_size) for s in stages])
+
+
+def device_model_for(model, stages: Sequence | None = None,
+                     kernels: np.ndarray | None = None) -> DeviceModel:
+    """Cached DeviceModel for ``model`` (or for the given stage list /
+    explicit kernels).  The cache key fingerprints every parameter, so
+    in-place edits of StageParams (as the reference's tests do) are seen."""
+    require_cuda()
+    t = torch()
+    stages = list(model.stages if stages is None else stages)
+    k = model_kernels(model, stages) if kernels is None else kernels
+    w = np.stack([np.asarray(s.weights, dtype=np.float64) for s in stages])
+    lams = np.array([math.exp(float(s.beta)) for s in stages])
+    g = model.rbf
+    grid = rbf_grid_params(g.count, g.radius, g.bandwidth)
+    dev = t.cuda.current_device()
+    key = (dev, params_fingerprint(model.filter_size, k, w, lams, grid))
+    cache = model.__dict__.setdefault("_tnrd_device_cache", {})
+    dm = cache.get(key)
+    if dm is None:
+        if len(cache) >= 8:
+            cache.pop(next(iter(cache))).close()
+        dm = cache[key] = DeviceModel(k, w, lams, grid, device=dev)
+    return dm

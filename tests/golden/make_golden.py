@@ -1,0 +1,144 @@
+"""Generate golden vectors by running the REAL reference (specklediff) here.
+
+Usage (in the build container, where /root/reference exists):
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+The reference cannot travel to the GPU box, so its outputs are committed
+as small .npz fixtures next to this script.  Each fixture holds the inputs
+(f as fp32-exact float64, model parameters) and the reference output, full
+for small cases and as border/centre crops plus global sums for the
+full-size BASELINE configs C1 and C2.
+"""
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import specklediff as sd  # noqa: E402  (the reference)
+from specklediff.diffusion import DiffusionModel, StageParams  # noqa: E402
+from specklediff.influence import RbfGrid  # noqa: E402
+
+from paper_1702_07482_b200 import synth  # noqa: E402
+
+CROP = 24
+
+
+def ref_model(m, nk, T, M, seed, weight_scale=0.1, beta=0.0, radius=310.0,
+              bandwidth=None, betas=None):
+    rng = np.random.default_rng(seed)
+    stages = []
+    for t in range(T):
+        c = rng.standard_normal((nk, m * m - 1))
+        c /= np.linalg.norm(c, axis=1, keepdims=True)
+        w = weight_scale * rng.standard_normal((nk, M))
+        b = beta if betas is None else betas[t]
+        stages.append(StageParams(beta=b, coeffs=c, weights=w))
+    grid = RbfGrid(count=M, radius=radius, bandwidth=bandwidth)
+    return DiffusionModel(stages=stages, filter_size=m, looks=1, rbf=grid)
+
+
+def pack_model(model):
+    return dict(
+        m=model.filter_size,
+        betas=np.array([s.beta for s in model.stages]),
+        coeffs=np.stack([s.coeffs for s in model.stages]),
+        weights=np.stack([s.weights for s in model.stages]),
+        rbf_count=model.rbf.count, rbf_radius=model.rbf.radius,
+        rbf_bandwidth=np.nan if model.rbf.bandwidth is None
+        else model.rbf.bandwidth)
+
+
+def crops(u):
+    H, W = u.shape
+    c = CROP
+    return dict(
+        crop_tl=u[:c, :c], crop_tr=u[:c, W - c:], crop_bl=u[H - c:, :c],
+        crop_br=u[H - c:, W - c:],
+        crop_c=u[H // 2 - c // 2:H // 2 + c // 2, W // 2 - c // 2:W // 2 + c // 2],
+        row_mid=u[H // 2], col_mid=u[:, W // 2],
+        sum=np.float64(u.sum()), sumsq=np.float64((u * u).sum()))
+
+
+def save(name, **kw):
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **kw)
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.1f} KiB)")
+
+
+def full_case(name, f, model, clean=None, full=True):
+    f = np.asarray(f, dtype=np.float32).astype(np.float64)
+    t0 = time.time()
+    u, _ = sd.run_diffusion(f, model)
+    dt = time.time() - t0
+    extra = {}
+    if clean is not None:
+        extra["clean"] = clean if full else np.float64(0)
+        extra["psnr"] = np.float64(sd.psnr(u, clean, 255.0))
+    out = dict(u=u) if full else crops(u)
+    save(name, f=f if full else np.float64(0), full=np.bool_(full),
+         f_sum=np.float64(f.sum()), f_crop=f[:CROP, :CROP],
+         ref_seconds=np.float64(dt), **pack_model(model), **out, **extra)
+
+
+def main(which):
+    rng = np.random.default_rng(20260101)
+    if "small" in which:
+        # reference test conventions (tests/test_diffusion.py:12-22)
+        full_case("small_m3", rng.uniform(1, 200, (16, 16)),
+                  ref_model(3, 3, 2, 9, seed=11, weight_scale=0.05))
+        full_case("ragged_m7", rng.uniform(0, 255, (37, 53)),
+                  ref_model(7, 5, 2, 63, seed=12))
+        full_case("tiny_m7", rng.uniform(1, 255, (4, 5)),
+                  ref_model(7, 4, 1, 63, seed=13))
+        full_case("m9", rng.uniform(1, 255, (33, 29)),
+                  ref_model(9, 6, 2, 63, seed=14))
+        full_case("m5_nk24", rng.uniform(1, 255, (40, 44)),
+                  ref_model(5, 24, 3, 63, seed=15))
+        full_case("m3_M7_nk1", rng.uniform(0, 255, (12, 12)),
+                  ref_model(3, 1, 3, 7, seed=16, weight_scale=0.05,
+                            betas=[0.3, -0.2, 0.1]))
+        full_case("beta_varied", rng.uniform(1, 255, (24, 31)),
+                  ref_model(5, 8, 3, 63, seed=17, betas=[0.7, -1.1, 0.2]))
+        full_case("narrow_bw", rng.uniform(1, 255, (20, 20)),
+                  ref_model(5, 6, 2, 63, seed=18, bandwidth=7.0))
+        full_case("wide_bw", rng.uniform(1, 255, (20, 20)),
+                  ref_model(5, 6, 2, 63, seed=19, bandwidth=25.0))
+        fz = rng.uniform(0, 255, (30, 30))
+        fz[rng.uniform(size=fz.shape) < 0.1] = 0.0
+        full_case("zeros_in_f", fz, ref_model(7, 8, 2, 63, seed=20))
+        fl = rng.uniform(0, 2000, (28, 36))  # far outside the RBF grid
+        full_case("wide_range", fl, ref_model(7, 8, 2, 63, seed=21,
+                                              weight_scale=0.3))
+        # speckled synthetic crops with the BASELINE models
+        c2 = synth.CONFIGS["c2"]
+        clean, f = synth.noisy_image(c2, 0, 64, 64)
+        full_case("c2_crop64", f, ref_model(7, 48, 5, 63, seed=2), clean)
+        # primitive pins: conv2d and prox
+        img = rng.normal(size=(19, 23)) * 50
+        ks = {m: rng.normal(size=(m, m)) for m in (3, 5, 7, 9)}
+        save("conv2d", img=img, **{f"k{m}": k for m, k in ks.items()},
+             **{f"out{m}": sd.conv2d(img, k) for m, k in ks.items()})
+        ut = rng.uniform(-10, 10, (50, 40))
+        fp = rng.uniform(1e-3, 10, (50, 40))
+        save("prox", u_tilde=ut, f=fp,
+             **{f"out_{i}": sd.prox_idiv(ut, fp, lam)
+                for i, lam in enumerate((0.01, 0.3, 1.0, 10.0))},
+             lams=np.array([0.01, 0.3, 1.0, 10.0]))
+    for key in ("c1", "c2"):
+        if key in which:
+            cfg = synth.CONFIGS[key]
+            clean, f = synth.noisy_image(cfg, 0)
+            model = ref_model(cfg.m, cfg.nk, cfg.T, cfg.M, seed=cfg.index)
+            full_case(f"{key}_full", f, model, clean, full=False)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["small", "c1", "c2"])

@@ -1,0 +1,108 @@
+"""CPU-only checks of the boundary: libtnrd.so loads, exports every symbol
+include/tnrd.h declares, the ctypes table agrees with the header, and the
+product path fails loudly without a GPU (no CPU fallback)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_1702_07482_b200 import _lib
+
+
+def header_functions():
+    src = open(_lib.HEADER_PATH).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tnrd_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_matches_binding_table():
+    assert header_functions() == sorted(_lib.SIGNATURES)
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.load()
+    for name in header_functions():
+        assert hasattr(L, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\sT\s(tnrd_[a-z0-9_]+)", out))
+    assert set(header_functions()) <= exported
+
+
+def test_library_is_built_for_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_library_does_not_link_the_oracle():
+    out = subprocess.run(["nm", "-D", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "oracle_" not in out
+    ldd = subprocess.run(["ldd", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "oracle" not in ldd
+
+
+def test_version_and_error_channel():
+    L = _lib.load()
+    assert b"sm_100a" in L.tnrd_version()
+    # host-side validation runs without a GPU
+    h = ctypes.c_void_p()
+    k = np.zeros((1, 1, 4, 4))
+    w = np.zeros((1, 1, 7))
+    lam = np.ones(1)
+    rc = L.tnrd_model_create(4, 1, 1, 7, _lib.dptr(k), _lib.dptr(w), -310.0,
+                             103.3, 103.3, _lib.dptr(lam), 0, ctypes.byref(h))
+    assert rc == _lib.TNRD_EINVAL
+    assert "odd" in _lib.last_error()
+    with pytest.raises(ValueError, match="odd"):
+        _lib.check(rc)
+    lam0 = np.zeros(1)
+    k3 = np.zeros((1, 1, 3, 3))
+    rc = L.tnrd_model_create(3, 1, 1, 7, _lib.dptr(k3), _lib.dptr(w), -310.0,
+                             103.3, 103.3, _lib.dptr(lam0), 0, ctypes.byref(h))
+    assert rc == _lib.TNRD_EINVAL and "lambda must be positive" in _lib.last_error()
+    rc = L.tnrd_model_create(11, 1, 1, 7, _lib.dptr(np.zeros((1, 1, 11, 11))),
+                             _lib.dptr(w), -310.0, 103.3, 103.3, _lib.dptr(lam),
+                             0, ctypes.byref(h))
+    assert rc == _lib.TNRD_EUNSUPPORTED
+
+
+def test_status_decode_maps_errors():
+    L = _lib.load()
+    bad = ctypes.c_int(0)
+    ok = (ctypes.c_uint32 * 2)(0xFFFFFFFF, 0xFFFFFFFF)
+    assert L.tnrd_status_decode(ok, ctypes.byref(bad)) == 0 and bad.value == -1
+    st = (ctypes.c_uint32 * 2)(3, 0xFFFFFFFF)
+    assert L.tnrd_status_decode(st, ctypes.byref(bad)) == _lib.TNRD_ENONFINITE
+    assert bad.value == 3
+    with pytest.raises(FloatingPointError, match="non-finite image after stage 3"):
+        _lib.check(_lib.TNRD_ENONFINITE)
+    neg = (ctypes.c_uint32 * 2)(0xFFFFFFFF, 0xFFFFFFFF & ~0x2)
+    assert L.tnrd_status_decode(neg, ctypes.byref(bad)) == _lib.TNRD_EINVAL
+    assert "nonnegative" in _lib.last_error()
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_1702_07482_b200 as tn
+    from paper_1702_07482_b200 import synth
+    model = synth.make_model(3, 2, 1, 7)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        tn.run_diffusion(np.ones((8, 8)), model)
+
+
+def test_product_package_never_imports_oracle():
+    pkg = os.path.dirname(os.path.abspath(_lib.__file__))
+    for root, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(root, fn)).read()
+                assert "import oracle" not in src and "from oracle" not in src, fn
+                assert "libtnrd_oracle" not in src, fn

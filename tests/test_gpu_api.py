@@ -1,0 +1,243 @@
+"""The reference's hot-path unit tests, restated against the GPU drop-in.
+
+Mirrors /root/reference/pkg/tests/test_diffusion.py, test_imageops.py,
+test_speckle.py and test_acceptance.py gates 1 and 4, with tolerances
+widened from float64 round-off to the fp32 parity bar where the GPU
+computes in fp32."""
+import math
+
+import numpy as np
+import pytest
+
+import paper_1702_07482_b200 as tn
+from paper_1702_07482_b200 import _lib, synth
+
+pytestmark = pytest.mark.gpu
+
+
+def make_model(rng, m=3, nk=2, T=1, M=7, beta=0.0, weight_scale=0.05):
+    # reference tests/test_diffusion.py:12-22
+    grid = tn.RbfGrid(count=M, radius=310.0)
+    stages = []
+    for _ in range(T):
+        c = rng.standard_normal((nk, m * m - 1))
+        c /= np.linalg.norm(c, axis=1, keepdims=True)
+        w = weight_scale * rng.standard_normal((nk, M))
+        stages.append(tn.StageParams(beta=beta, coeffs=c, weights=w))
+    return tn.DiffusionModel(stages=stages, filter_size=m, looks=4, rbf=grid)
+
+
+def zero_weight_model(rng, beta, T=1):
+    model = make_model(rng, T=T, beta=beta)
+    for s in model.stages:
+        s.weights[:] = 0.0
+    return model
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b) / np.abs(b)))
+
+
+# ------------------------------------------------------------- diffusion_step
+
+def test_zero_weights_reduces_to_prox(cuda, oracle):
+    rng = np.random.default_rng(2)
+    model = zero_weight_model(rng, beta=0.5)
+    f = rng.uniform(1, 10, (12, 12)).astype(np.float32).astype(np.float64)
+    u = rng.uniform(1, 10, (12, 12)).astype(np.float32).astype(np.float64)
+    out, trace = tn.diffusion_step(u, f, model.stages[0], model)
+    np.testing.assert_array_equal(trace.u_tilde, u)  # force is exactly 0
+    assert rel(out, oracle.prox_idiv(u, f, math.exp(0.5))) < 1e-6
+
+
+def test_zero_weights_tiny_lambda_is_identity(cuda):
+    rng = np.random.default_rng(3)
+    model = zero_weight_model(rng, beta=-40.0)
+    f = rng.uniform(1, 10, (12, 12))
+    u = rng.uniform(1, 10, (12, 12)).astype(np.float32).astype(np.float64)
+    out, _ = tn.diffusion_step(u, f, model.stages[0], model)
+    assert np.abs(out - u).max() < 1e-5
+
+
+def test_compositional_oracle(cuda, oracle):
+    rng = np.random.default_rng(4)
+    model = make_model(rng, nk=3, M=9)
+    stage = model.stages[0]
+    f = rng.uniform(1, 200, (16, 16)).astype(np.float32).astype(np.float64)
+    u = rng.uniform(1, 200, (16, 16)).astype(np.float32).astype(np.float64)
+    out, trace = tn.diffusion_step(u, f, stage, model)
+    kern = stage.kernels(model.basis, model.filter_size)
+    g = model.rbf
+    expected = oracle.stage(u, f, kern, stage.weights, g.centers, g.gamma, stage.lam)
+    assert rel(out, expected) < 1e-5
+    force = oracle.force(u, kern, stage.weights, g.centers, g.gamma)
+    assert np.abs(trace.u_tilde - (u - force)).max() < 1e-4 * np.abs(u).max()
+    # diffusion_force with explicit kernels
+    fgpu, z, phi, design = tn.diffusion_force(u, stage, kern, model.rbf)
+    assert z is None and phi is None and design is None
+    assert np.abs(fgpu - force).max() < 1e-4 * max(1.0, np.abs(force).max())
+
+
+def test_constant_image_closed_form(cuda):
+    rng = np.random.default_rng(5)
+    lam = math.exp(0.3)
+    model = zero_weight_model(rng, beta=0.3)
+    c = 4.0
+    out, _ = tn.run_diffusion(np.full((8, 8), c), model)
+    expected = (c + math.sqrt(c * c + 8 * (1 + 2 * lam) * lam * c * c)) / (2 * (1 + 2 * lam))
+    assert np.abs(out - expected).max() < 1e-5 * expected
+
+
+def test_positivity_and_determinism(cuda):
+    # reference test_diffusion.py:129-137 and acceptance gate 4 (:125-139)
+    rng = np.random.default_rng(404)
+    for trial in range(100):
+        T = int(rng.integers(1, 4))
+        nk = int(rng.integers(1, 5))
+        model = make_model(rng, m=3, nk=nk, T=T, M=7, beta=float(rng.normal(0.0, 0.5)))
+        side = int(rng.integers(8, 17))
+        f = rng.uniform(0.0, 255.0, (side, side))
+        out1, _ = tn.run_diffusion(f, model)
+        out2, _ = tn.run_diffusion(f, model)
+        assert np.all(out1 > 0.0)
+        np.testing.assert_array_equal(out1, out2)
+
+
+def test_prefix_invariance(cuda):
+    # reference test_diffusion.py:139-148, through the stage API
+    rng = np.random.default_rng(7)
+    model = make_model(rng, T=3)
+    f = rng.uniform(1, 255, (10, 10))
+    u0 = np.maximum(f, 1e-6)
+    u1, _ = tn.diffusion_step(u0, f, model.stages[0], model)
+    model.stages[2].weights += 0.1
+    model.stages[2].beta += 0.5
+    u1b, _ = tn.diffusion_step(u0, f, model.stages[0], model)
+    np.testing.assert_array_equal(u1, u1b)
+
+
+def test_in_place_param_edit_invalidates_device_cache(cuda):
+    rng = np.random.default_rng(8)
+    model = make_model(rng, T=2)
+    f = rng.uniform(1, 255, (10, 10))
+    a, _ = tn.run_diffusion(f, model)
+    model.stages[1].weights *= 3.0
+    b, _ = tn.run_diffusion(f, model)
+    assert not np.array_equal(a, b)
+
+
+# ------------------------------------------------------------- error contract
+
+def test_errors_match_reference(cuda):
+    rng = np.random.default_rng(9)
+    model = make_model(rng, m=7, nk=2)
+    with pytest.raises(ValueError, match="nonnegative"):
+        tn.run_diffusion(-np.ones((10, 10)), model)
+    bad = np.ones((10, 10))
+    bad[3, 3] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        tn.run_diffusion(bad, model)
+    with pytest.raises(ValueError, match="2D"):
+        tn.run_diffusion(np.ones(10), model)
+    with pytest.raises(ValueError, match="degenerate"):
+        tn.run_diffusion(np.ones((2, 2)), model)
+    with pytest.raises(NotImplementedError):
+        tn.run_diffusion(np.ones((10, 10)), model, keep_traces=True)
+
+
+def test_nonfinite_stage_raises_floating_point_error(cuda):
+    model = synth.make_model(3, 2, 3, 7, seed=1, weight_scale=1e30)
+    f = np.random.default_rng(0).uniform(1, 255, (40, 40))
+    with pytest.raises(FloatingPointError, match="non-finite image after stage 0"):
+        tn.run_diffusion(f, model)
+
+
+def test_device_entry_validates_f(cuda):
+    torch = cuda
+    model = synth.make_model(5, 4, 2, 63, seed=2)
+    f = torch.rand(2, 20, 20, device="cuda") * 100
+    f[1, 5, 5] = -1.0
+    with pytest.raises(ValueError, match="nonnegative"):
+        tn.run_diffusion_batch(f, model)
+    f[1, 5, 5] = float("inf")
+    with pytest.raises(ValueError, match="non-finite"):
+        tn.run_diffusion_batch(f, model)
+
+
+# ------------------------------------------------------------- primitives
+
+def _mirror(j, n):
+    return -1 - j if j < 0 else (2 * n - 1 - j if j >= n else j)
+
+
+def test_conv2d_bruteforce_and_golden(cuda):
+    from conftest import load_golden
+    rng = np.random.default_rng(2)
+    img = rng.normal(size=(16, 16))
+    k = rng.normal(size=(5, 5))
+    ref = np.zeros_like(img)
+    for i in range(16):
+        for j in range(16):
+            ref[i, j] = sum(k[2 + p, 2 + q] * img[_mirror(i - p, 16), _mirror(j - q, 16)]
+                            for p in range(-2, 3) for q in range(-2, 3))
+    assert np.abs(tn.conv2d(img, k) - ref).max() < 1e-5
+    g = load_golden("conv2d")
+    for m in (3, 5, 7, 9):
+        out = tn.conv2d(g["img"], g[f"k{m}"])
+        assert np.abs(out - g[f"out{m}"]).max() < 1e-5 * np.abs(g[f"out{m}"]).max()
+    delta = np.zeros((5, 5))
+    delta[2, 2] = 1.0
+    img = rng.normal(size=(9, 13)).astype(np.float32).astype(np.float64)
+    np.testing.assert_array_equal(tn.conv2d(img, delta), img)
+    with pytest.raises(ValueError):
+        tn.conv2d(np.zeros((4, 4)), np.zeros((11, 11)))
+    with pytest.raises(ValueError):
+        tn.conv2d(np.zeros((4, 4)), np.zeros((4, 4)))
+
+
+def golden_section_prox(u_tilde, f, lam, tol=1e-9):
+    def obj(u):
+        return 0.5 * (u - u_tilde) ** 2 + lam * (u * u - 2 * f * f * math.log(u))
+    a, b = 1e-12, abs(u_tilde) + 3.0 * f + 10.0
+    phi = (math.sqrt(5.0) - 1.0) / 2.0
+    c, d = b - phi * (b - a), a + phi * (b - a)
+    fc, fd = obj(c), obj(d)
+    while b - a > tol:
+        if fc < fd:
+            b, d, fd = d, c, fc
+            c = b - phi * (b - a)
+            fc = obj(c)
+        else:
+            a, c, fc = c, d, fd
+            d = a + phi * (b - a)
+            fd = obj(d)
+    return 0.5 * (a + b)
+
+
+def test_prox_known_value_minimizer_and_golden(cuda):
+    from conftest import load_golden
+    out = tn.prox_idiv(np.array([[2.0]]), np.array([[3.0]]), 1.0)
+    assert abs(out[0, 0] - (2.0 + math.sqrt(220.0)) / 6.0) < 1e-6
+    rng = np.random.default_rng(5)
+    ut = rng.uniform(-10, 10, (100, 100))
+    f = rng.uniform(1e-6, 10, (100, 100))
+    for lam in (0.01, 1.0, 10.0):
+        assert np.all(tn.prox_idiv(ut, f, lam) > 0)
+    for _ in range(200):
+        u_, f_, l_ = rng.uniform(-10, 10), rng.uniform(1e-3, 10), rng.uniform(1e-3, 10)
+        closed = tn.prox_idiv(np.array([[u_]]), np.array([[f_]]), l_)[0, 0]
+        assert abs(closed - golden_section_prox(u_, f_, l_)) < 1e-5 * max(1.0, closed)
+    g = load_golden("prox")
+    for i, lam in enumerate(g["lams"]):
+        o = tn.prox_idiv(g["u_tilde"], g["f"], float(lam))
+        assert np.max(np.abs(o - g[f"out_{i}"]) / g[f"out_{i}"]) < 1e-5
+    with pytest.raises(ValueError):
+        tn.prox_idiv(np.ones((2, 2)), np.ones((2, 2)), 0.0)
+
+
+def test_launch_counter_counts_stages(cuda):
+    model = synth.make_model(7, 8, 4, 63, seed=9)
+    f = np.random.default_rng(0).uniform(1, 255, (40, 40))
+    _lib.launch_count_reset()
+    tn.run_diffusion(f, model)
+    assert _lib.launch_count() == 4
