@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 TNRD despeckling path (contract: see DESIGN.md §Bench).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c5]
+                    [--impl ours|reference]
+
+A step = one full despeckle (T fused stages) of one batch of the workload.
+Default workload = BASELINE.json configs[1] (C2: one 512x512 image, 7x7,
+Nk=48, T=5).  Under torchrun each rank despeckles its own image(s) (C2:
+weak scaling, one image per rank; C3/C5: the batch split over ranks,
+strong scaling); no data-path collective.  Rank 0 prints ONE JSON line.
+
+--impl reference times the reference's CPU algorithm: the reference is pure
+Python/numpy and cannot travel to the GPU box, so the float64 C port in
+oracle/ (pinned bit-for-bit-ish to the reference's golden vectors, see
+tests/test_oracle.py) runs with every host thread on a bounded sample of
+the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = ("megapixels/sec for full TNRD despeckle (7×7, 48 filters, "
+          "5 stages) at 1/2/4/8 B200")
+UNIT = "MPix/s"
+
+
+def w_flop(cfg) -> int:
+    """algorithmic FLOP per pixel-stage (FMA = 2)."""
+    return 4 * cfg.nk * cfg.m * cfg.m + 5 * cfg.nk * cfg.M + 10
+
+
+def w_sfu(cfg) -> int:
+    return cfg.nk * cfg.M + 2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU baseline
+
+def cpu_reference_run(cfg, model, f, budget_s: float):
+    """Time the float64 C port of the reference algorithm (all host
+    threads) on f, shrinking to a centred crop if a run exceeds budget_s.
+    Returns (mpix_per_s, seconds, sample_desc, threads)."""
+    from oracle import oracle as O
+    O.build()
+    O.set_threads(-1)
+    threads = O.threads()
+    H, W = f.shape
+    side = min(H, W)
+    while True:
+        y0, x0 = (H - side) // 2, (W - side) // 2
+        crop = f[y0:y0 + side, x0:x0 + side].astype(np.float64)
+        t0 = time.perf_counter()
+        O.run_diffusion(crop, model)
+        dt = time.perf_counter() - t0
+        if dt <= budget_s or side <= 64:
+            break
+        side = max(64, int(side * (budget_s / dt) ** 0.5 * 0.9) // 8 * 8)
+    sample = (f"{side}x{side} crop of image 0 ({'full image' if side == min(H, W) and H == W else 'bounded sample'}), "
+              f"{cfg.m}x{cfg.m}, Nk={cfg.nk}, T={cfg.T}, float64 C port of the reference "
+              f"algorithm (oracle/tnrd_oracle.c), {threads} threads")
+    return side * side / dt / 1e6, dt, sample, threads
+
+
+def run_reference_arm(args, cfg, rank):
+    if rank != 0:
+        return
+    from paper_1702_07482_b200 import synth
+    model = synth.config_model(cfg)
+    _, f = synth.noisy_image(cfg, 0)
+    per_step = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    rate, dt, sample, threads = cpu_reference_run(cfg, model, f, per_step)
+    from oracle import oracle as O
+    side = int(round((rate * 1e6 * dt) ** 0.5))
+    y0 = (cfg.H - side) // 2
+    crop = f[y0:y0 + side, y0:y0 + side].astype(np.float64)
+    for _ in range(max(0, args.warmup - 1)):
+        O.run_diffusion(crop, model)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.run_diffusion(crop, model)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = side * side / (ms * 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(cfg, args, per_rank_batch=1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- ours
+
+def workload_config(cfg, args, per_rank_batch):
+    return {
+        "workload": f"{cfg.name}: {cfg.note}",
+        "H": cfg.H, "W": cfg.W, "filter_size": cfg.m, "num_filters": cfg.nk,
+        "stages": cfg.T, "rbf_centres": cfg.M, "images_per_rank": per_rank_batch,
+        "parallelism": f"{'replicas' if cfg.batch == 1 else 'batch-sharded'} x{args.gpus}",
+        "l2": "256 MiB L2-flush write between timed steps, outside the per-step CUDA events",
+        "inputs": "seeded piecewise-smooth clean x Philox amplitude speckle (synth.py)",
+    }
+
+
+def measure_peaks(torch, L, stream):
+    """FFMA (TFLOP/s) and MUFU ex2 (Gop/s) peaks measured on this GPU."""
+    out = {}
+    for kind, key in ((0, "fp32_tflops"), (1, "mufu_ex2_gops")):
+        ops = ctypes.c_double(0)
+        iters = 20000 if kind == 0 else 8000
+        for _ in range(2):
+            L.tnrd_probe(kind, iters, 4, ctypes.c_void_p(stream.cuda_stream), ctypes.byref(ops))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        best = 0.0
+        for _ in range(3):
+            e0.record(stream)
+            L.tnrd_probe(kind, iters, 4, ctypes.c_void_p(stream.cuda_stream), ctypes.byref(ops))
+            e1.record(stream)
+            e1.synchronize()
+            best = max(best, ops.value / (e0.elapsed_time(e1) * 1e-3))
+        out[key] = best / (1e12 if kind == 0 else 1e9)
+    return out
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    from paper_1702_07482_b200 import synth
+    cfg = synth.CONFIGS[args.workload]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg, rank)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1702_07482_b200 as tn
+    from paper_1702_07482_b200 import _lib
+
+    L = _lib.load()
+    model = synth.config_model(cfg)
+    if cfg.batch == 1:
+        idx = [rank]                      # C2: one image per rank (weak)
+    else:
+        per = cfg.batch // world          # C3/C5: batch sharded (strong)
+        idx = list(range(rank * per, (rank + 1) * per))
+    B = len(idx)
+    f_host = np.stack([synth.noisy_image(cfg, i)[1] for i in idx])
+    dm = tn.device_model_for(model)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(dev)
+    f = torch.from_numpy(f_host).to(dev)
+    out = torch.empty_like(f)
+    work = torch.empty_like(f)
+    status = tn.engine.Status(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    H, W = cfg.H, cfg.W
+    sh = ctypes.c_void_p(stream.cuda_stream)
+    bufs = [out, work]
+
+    def step(evs=None):
+        # T fused stage launches through the C ABI; final stage lands in `out`
+        L.tnrd_status_reset(ctypes.c_void_p(status.buf.data_ptr()), sh)
+        cur = f
+        for t in range(cfg.T):
+            dst = out if (cfg.T - 1 - t) % 2 == 0 else work
+            fl = (_lib.STAGE_FLOOR_INPUT | _lib.STAGE_CHECK_F) if t == 0 else 0
+            if evs is not None:
+                evs[t].record(stream)
+            rc = L.tnrd_stage(dm.handle, t, ctypes.c_void_p(cur.data_ptr()),
+                              ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(dst.data_ptr()),
+                              B, H, W, W, H * W, fl, ctypes.c_void_p(status.buf.data_ptr()), sh)
+            if rc:
+                _lib.check(rc)
+            cur = dst
+        if evs is not None:
+            evs[cfg.T].record(stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, args.warmup)):
+            step()
+            flush.zero_()
+        stream.synchronize()
+        status.check()
+        peaks = measure_peaks(torch, L, stream)
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        smi_index = int(vis.split(",")[local]) if vis and vis.split(",")[local].isdigit() else local
+        clocks = ClockSampler(smi_index)
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(cfg.T + 1)]
+               for _ in range(args.steps)]
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        clocks.start()
+        _lib.launch_count_reset()
+        for k in range(args.steps):
+            step(evs[k])
+            flush.zero_()                 # outside the events: L2 flush
+        torch.cuda.synchronize(dev)
+        launches = _lib.launch_count()
+        if dist is not None:
+            dist.barrier()
+        clk = clocks.stop()
+        status.check()
+
+    step_ms = [evs[k][0].elapsed_time(evs[k][cfg.T]) for k in range(args.steps)]
+    stage_ms = [evs[k][t].elapsed_time(evs[k][t + 1])
+                for k in range(args.steps) for t in range(cfg.T)]
+    ms = sum(step_ms) / len(step_ms)
+    launch_ms = sum(stage_ms) / len(stage_ms)
+    if dist is not None:
+        tt = torch.tensor([ms, launch_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, launch_ms = tt.tolist()
+
+    px_rank = B * H * W
+    value = world * px_rank / (ms * 1e3)          # MPix/s, all ranks
+
+    # ---- e2e: reference-facing call with HOST buffers (pinned), through the
+    # plan C ABI (H2D + T stages + D2H + status check in the timed region)
+    pin_f = torch.from_numpy(f_host).pin_memory()
+    pin_u = torch.empty_like(pin_f).pin_memory()
+    plan = dm._plan(B, H, W)
+    pstream = torch.cuda.ExternalStream(L.tnrd_plan_stream(plan), device=dev)
+    for _ in range(3):
+        _lib.check(L.tnrd_plan_despeckle_host(plan, ctypes.c_void_p(pin_f.data_ptr()),
+                                              ctypes.c_void_p(pin_u.data_ptr())))
+    e2e_steps = max(3, min(args.steps, 50))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    if dist is not None:
+        dist.barrier()
+    e0.record(pstream)
+    for _ in range(e2e_steps):
+        _lib.check(L.tnrd_plan_despeckle_host(plan, ctypes.c_void_p(pin_f.data_ptr()),
+                                              ctypes.c_void_p(pin_u.data_ptr())))
+    e1.record(pstream)
+    e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if dist is not None:
+        tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = tt.item()
+    assert np.array_equal(pin_u.numpy(), out.cpu().numpy()), "e2e result differs"
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the fused stage kernel (SURVEY 8(d) algorithmic work)
+    px_launch = px_rank
+    flop_launch = w_flop(cfg) * px_launch
+    sfu_launch = w_sfu(cfg) * px_launch
+    achieved_tf = flop_launch / (launch_ms * 1e-3) / 1e12
+    peak_tf = peaks["fp32_tflops"]
+    peak_sfu = peaks["mufu_ex2_gops"] * 1e9
+    t_roof = max(w_flop(cfg) / (peak_tf * 1e12), w_sfu(cfg) / peak_sfu)  # s per pixel-stage
+    roof_pxst = 1.0 / t_roof / 1e6                                        # MPix*stages/s
+    ach_pxst = px_launch / (launch_ms * 1e-3) / 1e6
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(cfg.name)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak" if cfg.batch == 1 else "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(cfg, args, B),
+        "roofline": {
+            "bound": "fp32", "unit": "TFLOP/s", "achieved": achieved_tf,
+            "peak": peak_tf, "frac": achieved_tf / peak_tf, "traffic": traffic,
+            "peak_source": "measured on this GPU by tnrd_probe (FFMA); MEASURED_PEAKS.json has no FP32/MUFU entry",
+            "work": f"SURVEY 8(d): W_flop={w_flop(cfg)} FLOP/pixel-stage x {px_launch} px per launch",
+            "launch_ms": launch_ms,
+            "survey_combined": {
+                "unit": "MPix*stages/s", "achieved": ach_pxst, "peak": roof_pxst,
+                "frac": ach_pxst / roof_pxst,
+                "rule": "t_roof = max(W_flop/P_fp32, W_sfu/P_mufu) with on-box P_fp32, P_mufu",
+                "p_mufu_gops": peaks["mufu_ex2_gops"]},
+        },
+        "e2e": {"value": world * px_rank / (e2e_ms * 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": int(f_host.nbytes),
+                "d2h_bytes_per_step": int(f_host.nbytes) + 8,
+                "path": "tnrd_plan_despeckle_host (C ABI), pinned host buffers"},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        per = 20.0
+        rate, dt, sample, threads = cpu_reference_run(cfg, model, f_host[0], per)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads,
+                                "kind": "port", "sample": sample}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

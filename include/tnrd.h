@@ -77,9 +77,15 @@ int tnrd_model_create(int m, int nk, int T, int M, const double* kernels,
                       double gamma, const double* lam, int device,
                       tnrd_model** out);
 int tnrd_model_destroy(tnrd_model* model);
-/* m, nk, T, M, rbf path (1 = windowed Horner, 0 = direct all-centre sum) */
+/* m, nk, T, M, rbf path (1 = piecewise-polynomial table, 0 = direct
+ * all-centre sum) */
 int tnrd_model_info(const tnrd_model* model, int* m, int* nk, int* T, int* M,
                     int* fast_rbf);
+/* Accuracy of the polynomial RBF tables built at creation: max |p - phi|
+ * over every interval/filter/stage (fp32-rounded coefficients, float64
+ * evaluation), the largest sum_j |w_ij|, and the interval count. */
+int tnrd_model_rbf_fit(const tnrd_model* model, double* max_abs_err,
+                       double* max_sum_abs_w, int* intervals);
 
 /* Reset a device status block (stream-ordered memset). */
 int tnrd_status_reset(uint32_t* d_status, void* stream);
@@ -135,6 +141,12 @@ int tnrd_prox_idiv(const float* u_tilde, const float* f, float* out,
  * the last reset (instrumentation for bench.py's gpu_launches). */
 uint64_t tnrd_launch_count(void);
 void tnrd_launch_count_reset(void);
+
+/* Peak probes for the roofline denominators (not on the reference's path):
+ * kind 0 = FP32 FFMA, 1 = MUFU ex2.  Launches one saturating kernel on
+ * `stream` and returns its operation count in *ops (FLOP for kind 0). */
+int tnrd_probe(int kind, int iters, int blocks_per_sm, void* stream,
+               double* ops);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

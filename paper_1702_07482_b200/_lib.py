@@ -45,6 +45,9 @@ SIGNATURES = {
                                    ctypes.POINTER(_vp)]),
     "tnrd_model_destroy": (_c_int, [_vp]),
     "tnrd_model_info": (_c_int, [_vp] + [ctypes.POINTER(_c_int)] * 5),
+    "tnrd_model_rbf_fit": (_c_int, [_vp, ctypes.POINTER(_c_dbl),
+                                    ctypes.POINTER(_c_dbl),
+                                    ctypes.POINTER(_c_int)]),
     "tnrd_status_reset": (_c_int, [_vp, _vp]),
     "tnrd_status_decode": (_c_int, [ctypes.POINTER(_c_u32),
                                     ctypes.POINTER(_c_int)]),
@@ -66,6 +69,8 @@ SIGNATURES = {
     "tnrd_prox_idiv": (_c_int, [_vp, _vp, _vp, _c_i64, _c_dbl, _vp]),
     "tnrd_launch_count": (ctypes.c_uint64, []),
     "tnrd_launch_count_reset": (None, []),
+    "tnrd_probe": (_c_int, [_c_int, _c_int, _c_int, _vp,
+                            ctypes.POINTER(ctypes.c_double)]),
 }
 
 _lib = None

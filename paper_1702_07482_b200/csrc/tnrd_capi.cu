@@ -66,14 +66,64 @@ extern "C" void tnrd_launch_count_reset(void) { g_launches.store(0); }
 struct tnrd_model {
     int m = 0, nk = 0, nk_pad = 0, T = 0, M = 0;
     int device = 0;
-    bool fast = false;
+    bool fast = false;   // polynomial RBF table (else direct all-centre sum)
     int kp = 0;          // floats per filter in taps
     int tab_stride = 0;  // floats per filter in tab
     double mu0 = 0, delta = 0, gamma = 0;
+    double zlo = 0, h = 0;  // polynomial intervals: centre j at zlo + j h
+    int ni = 0;             // number of intervals
+    double fit_err = 0;     // max |p(z) - phi(z)| over all filters/stages
+    double fit_scale = 0;   // max sum_j |w_ij|
     std::vector<double> lam;
     float* d_taps = nullptr;  // T * nk_pad * kp
     float* d_tab = nullptr;   // T * nk_pad * tab_stride
 };
+
+// phi(z) of one filter, as the reference evaluates it (influence.py:40-45)
+static double phi_exact(const double* w, int M, double mu0, double delta, double gamma, double z) {
+    double s = 0.0;
+    for (int j = 0; j < M; ++j) {
+        const double d = z - (mu0 + j * delta);
+        s += w[j] * std::exp(-d * d / (2.0 * gamma * gamma));
+    }
+    return s;
+}
+
+// Degree-11 interpolant of phi on [zc - h/2, zc + h/2] at Chebyshev nodes,
+// as monomial coefficients in x = (z - zc)/h.  Returns the max abs error of
+// the fp32-rounded coefficients over 41 check points.
+static double fit_interval(const double* w, int M, double mu0, double delta, double gamma,
+                           double zc, double h, float* out) {
+    constexpr int N = kPolyDeg + 1;
+    long double A[N][N + 1];
+    for (int k = 0; k < N; ++k) {
+        const long double x = 0.5L * std::cos(M_PI * (2 * k + 1) / (2.0 * N));
+        long double xp = 1.0L;
+        for (int d = 0; d < N; ++d) { A[k][d] = xp; xp *= x; }
+        A[k][N] = phi_exact(w, M, mu0, delta, gamma, zc + (double)x * h);
+    }
+    for (int c = 0; c < N; ++c) {  // Gaussian elimination, partial pivoting
+        int piv = c;
+        for (int r = c + 1; r < N; ++r)
+            if (std::fabs((double)A[r][c]) > std::fabs((double)A[piv][c])) piv = r;
+        if (piv != c)
+            for (int k = 0; k <= N; ++k) std::swap(A[c][k], A[piv][k]);
+        for (int r = 0; r < N; ++r) {
+            if (r == c) continue;
+            const long double f = A[r][c] / A[c][c];
+            for (int k = c; k <= N; ++k) A[r][k] -= f * A[c][k];
+        }
+    }
+    for (int d = 0; d < N; ++d) out[d] = (float)(A[d][N] / A[d][d]);
+    double err = 0.0;
+    for (int k = 0; k <= 40; ++k) {
+        const double x = -0.5 + k / 40.0;
+        double acc = 0.0;
+        for (int d = N - 1; d >= 0; --d) acc = acc * x + (double)out[d];
+        err = std::max(err, std::fabs(acc - phi_exact(w, M, mu0, delta, gamma, zc + x * h)));
+    }
+    return err;
+}
 
 static bool finite_all(const double* p, size_t n) {
     for (size_t i = 0; i < n; ++i)
@@ -108,17 +158,15 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
     md->mu0 = mu0; md->delta = delta; md->gamma = gamma;
     md->lam.assign(lam, lam + T);
     md->kp = round_up(m * m, 4);
-    // windowed Horner RBF is exact (to the truncation bound in DESIGN.md)
-    // when the Gaussians are no wider than the centre spacing and not so
-    // narrow that the window's power series leaves fp32 range.
-    const double rho = delta / gamma;
-    md->fast = rho >= 1.0 - 1e-9 && rho <= 2.0;
-    if (md->fast) {
-        const int ng = (M + kPadL) / 4 + 1;
-        md->tab_stride = ng * kWin;
-    } else {
-        md->tab_stride = round_up(M, 4);
-    }
+    // piecewise-polynomial RBF: intervals of width h = min(delta, gamma)
+    // (one Gaussian std or less, so degree 11 reaches ~1e-11 of sum|w|) over
+    // [mu_0 - 7 gamma, mu_{M-1} + 7 gamma]; beyond that phi < 3e-11 sum|w|.
+    md->h = std::min(delta, gamma);
+    md->zlo = mu0 - 7.0 * gamma;
+    const double zhi = mu0 + (M - 1) * delta + 7.0 * gamma;
+    md->ni = (int)std::ceil((zhi - md->zlo) / md->h) + 1;
+    md->fast = (size_t)md->ni * kPolyStride * kF <= 16384;  // <= 64 KB per group buffer
+    md->tab_stride = md->fast ? md->ni * kPolyStride : round_up(M, 4);
 
     const size_t ntap = (size_t)T * md->nk_pad * md->kp;
     const size_t ntab = (size_t)T * md->nk_pad * md->tab_stride;
@@ -131,16 +179,14 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
             const double* w = weights + ((size_t)t * nk + i) * M;
             float* tb = tab.data() + ((size_t)t * md->nk_pad + i) * md->tab_stride;
             if (md->fast) {
-                // A[g][k'] = w_{4g - P + k'} * exp(-(k'-8)^2 delta^2 / (2 gamma^2))
-                const int ng = md->tab_stride / kWin;
-                for (int g = 0; g < ng; ++g)
-                    for (int kq = 0; kq < kWin; ++kq) {
-                        const int j = 4 * g - kPadL + kq;
-                        const double wj = (j >= 0 && j < M) ? w[j] : 0.0;
-                        const double e = std::exp(-(double)((kq - 8) * (kq - 8)) * delta * delta /
-                                                  (2.0 * gamma * gamma));
-                        tb[g * kWin + kq] = (float)(wj * e);
-                    }
+                double sw = 0.0;
+                for (int j = 0; j < M; ++j) sw += std::fabs(w[j]);
+                md->fit_scale = std::max(md->fit_scale, sw);
+                for (int q = 0; q < md->ni; ++q)
+                    md->fit_err = std::max(md->fit_err,
+                                           fit_interval(w, M, mu0, delta, gamma,
+                                                        md->zlo + q * md->h, md->h,
+                                                        tb + q * kPolyStride));
             } else {
                 for (int j = 0; j < M; ++j) tb[j] = (float)w[j];
             }
@@ -180,6 +226,15 @@ extern "C" int tnrd_model_destroy(tnrd_model* md) {
     return TNRD_OK;
 }
 
+extern "C" int tnrd_model_rbf_fit(const tnrd_model* md, double* max_abs_err, double* max_sum_abs_w,
+                                  int* intervals) {
+    if (!md) return fail(TNRD_EINVAL, "model is NULL");
+    if (max_abs_err) *max_abs_err = md->fit_err;
+    if (max_sum_abs_w) *max_sum_abs_w = md->fit_scale;
+    if (intervals) *intervals = md->fast ? md->ni : 0;
+    return TNRD_OK;
+}
+
 extern "C" int tnrd_model_info(const tnrd_model* md, int* m, int* nk, int* T, int* M, int* fast) {
     if (!md) return fail(TNRD_EINVAL, "model is NULL");
     if (m) *m = md->m;
@@ -216,7 +271,7 @@ extern "C" int tnrd_status_decode(const uint32_t* h, int* bad_stage) {
 template <int MS, bool FAST>
 struct StageKernel {
     // tile choice per filter size
-    static constexpr int TH = 32, TW = 32, RF = 2, RB = 2, NT = 128;
+    static constexpr int TH = 32, TW = 32, RF = 2, RB = 2, NT = 256;
     using C = StageCfg<MS, TH, TW, RF, RB, NT>;
 
     static int launch(const StageArgs& a, int batch, cudaStream_t s) {
@@ -282,13 +337,10 @@ static int launch_stage(const tnrd_model* md, int t, const float* u_in, const fl
     a.c8 = (float)(8.0 * aa * lam);
     a.inv2a = (float)(1.0 / (2.0 * aa));
     const double L2E = 1.4426950408889634;
-    a.zlo = (float)(md->mu0 - 7.0 * md->delta);
-    a.zhi = (float)(md->mu0 + (md->M - 1 + 7) * md->delta);
-    a.inv_delta = (float)(1.0 / md->delta);
-    a.t_off = (float)(-md->mu0 / md->delta);
-    a.z_off = (float)(-md->mu0);
+    a.inv_h = (float)(1.0 / md->h);
+    a.t_off = (float)(-md->zlo / md->h);
+    a.tmax = (float)(md->ni - 1);
     a.delta = (float)md->delta;
-    a.cq = (float)(md->delta * L2E / (md->gamma * md->gamma));
     a.cE = (float)(-L2E / (2.0 * md->gamma * md->gamma));
     a.mu0 = (float)md->mu0;
     a.M = md->M;

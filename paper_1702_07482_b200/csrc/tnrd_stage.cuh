@@ -16,14 +16,15 @@
 //     are prefetched into shared memory with cp.async one group ahead;
 //   * forward pass: each work item = one filter x RF x 4 phi block; the 49
 //     taps live in registers, u rows are read as float4;
-//   * the RBF is evaluated exactly (to < 1e-9 relative to the weights) with
-//     a 16-centre window around z: phi = E(d) * [P+(q) + P-(1/q)], two
-//     Horner chains over a per-filter pre-scaled weight table, 3 ex2 per
-//     response instead of M=63;
+//   * the RBF phi_i is evaluated from a per-filter piecewise degree-11
+//     polynomial table (float64 Chebyshev fit on the host, error < 1e-10 of
+//     sum|w|): 3 conflict-free LDS.128 + 11 FFMA per response instead of
+//     M=63 exponentials;
 //   * phi halos that fall outside the image are filled by mirroring the
 //     in-image phi values (reference pads phi itself, diffusion.py:180);
-//   * backward pass: each thread owns an RB x 4 output block and keeps the
-//     force in registers across all filter groups;
+//   * backward pass: each thread owns an RB x 4 output block for half of
+//     the group's filters and keeps its partial force in registers across
+//     all groups; the two halves are summed once in the epilogue;
 //   * epilogue: u~ = u - force, cancellation-free prox, non-finite flag,
 //     f validation (stage 0), store.
 #pragma once
@@ -33,9 +34,8 @@
 namespace tnrd {
 
 constexpr int kF = 4;          // filters per group
-constexpr int kWin = 16;       // RBF window (centres) of the fast path
-constexpr int kPadL = 16;      // table padding (centres) left of mu_0
-constexpr int kHalfWin = 6;    // window must cover j0-6 .. j0+6
+constexpr int kPolyDeg = 11;   // RBF interpolant degree per interval
+constexpr int kPolyStride = 12;  // floats per interval (degree + 1)
 constexpr float kFFloor = 1e-6f;  // speckle.py:21
 
 __host__ __device__ constexpr int round_up(int x, int a) { return (x + a - 1) / a * a; }
@@ -55,16 +55,15 @@ struct StageArgs {
     float lam4;          // 4 lam
     float c8;            // 8 a lam
     float inv2a;         // 1 / (2a)
-    // RBF constants
-    float zlo, zhi;      // z clamp (fast path)
-    float inv_delta;     // 1 / delta
-    float t_off;         // -mu0 / delta
-    float z_off;         // -mu0
+    // RBF: polynomial table (default) -- t = z / h + t_off, clamp [0, tmax]
+    float inv_h;
+    float t_off;
+    float tmax;
+    // RBF: direct all-centre sum (fallback for very large tables)
     float delta;
-    float cq;            // delta * log2(e) / gamma^2
     float cE;            // -log2(e) / (2 gamma^2)
-    float mu0;           // generic path
-    int M;               // generic path: number of centres
+    float mu0;
+    int M;
     uint32_t flags;
     int stage;
     uint32_t* status;    // [0] first non-finite stage (atomicMin), [1] f flags (atomicAnd ~bit)
@@ -91,40 +90,33 @@ __device__ __forceinline__ int mirror_clamp(int j, int n) {
     return min(max(j, 0), n - 1);
 }
 
-// phi(z) with the windowed two-chain Horner form (fast path, gamma <= delta).
-//   window start (table index) ps = (j0 + kPadL - kHalfWin) & ~3, middle
-//   centre c = ps - kPadL + 8, d = z - mu_c, q = exp(delta d / gamma^2),
-//   E = exp(-d^2 / (2 gamma^2)), A[k'] = w_{c-8+k'} exp(-(k'-8)^2 delta^2 / (2 gamma^2)):
-//   phi = E * (sum_{k'>=8} A[k'] q^(k'-8) + sum_{k'<8} A[k'] (1/q)^(8-k'))
-__device__ __forceinline__ float rbf_fast(float z, const float* __restrict__ tabf,
+// phi(z) from the per-filter piecewise polynomial table (default path).
+//   The host samples phi_i(z) = sum_j w_ij exp(-(z-mu_j)^2/(2 gamma^2)) in
+//   float64 at 12 Chebyshev nodes of every interval of width h = min(delta,
+//   gamma) covering [mu_0 - 7 gamma, mu_{M-1} + 7 gamma] and stores the
+//   degree-11 interpolant's monomial coefficients in the local variable
+//   x in [-1/2, 1/2].  Interpolation error < 1e-10 * sum|w| (checked on the
+//   host at model creation); no MUFU, 3 LDS.128 + 11 FFMA.
+__device__ __forceinline__ float rbf_poly(float z, const float* __restrict__ tabf,
                                           const StageArgs& p) {
-    z = fminf(fmaxf(z, p.zlo), p.zhi);
-    const float t = fmaf(z, p.inv_delta, p.t_off);
-    const int j0 = __float_as_int(t + 12582912.0f) - 0x4B400000;  // rint(t)
-    const int ps = (j0 + (kPadL - kHalfWin)) & ~3;
-    const float fc = __int_as_float(ps + (0x4B400000 + 8 - kPadL)) - 12582912.0f;
-    const float d = fmaf(-p.delta, fc, z + p.z_off);
-    const float x = d * p.cq;
-    const float q = ex2f(x);
-    const float qi = ex2f(-x);
-    const float E = ex2f(d * d * p.cE);
-    const float4* A = reinterpret_cast<const float4*>(tabf + ps * 4);
-    const float4 a0 = A[0], a1 = A[1], a2 = A[2], a3 = A[3];
-    float hp = fmaf(a3.w, q, a3.z);
-    hp = fmaf(hp, q, a3.y);
-    hp = fmaf(hp, q, a3.x);
-    hp = fmaf(hp, q, a2.w);
-    hp = fmaf(hp, q, a2.z);
-    hp = fmaf(hp, q, a2.y);
-    hp = fmaf(hp, q, a2.x);
-    float hm = fmaf(a0.x, qi, a0.y);
-    hm = fmaf(hm, qi, a0.z);
-    hm = fmaf(hm, qi, a0.w);
-    hm = fmaf(hm, qi, a1.x);
-    hm = fmaf(hm, qi, a1.y);
-    hm = fmaf(hm, qi, a1.z);
-    hm = fmaf(hm, qi, a1.w);
-    return E * fmaf(hm, qi, hp);
+    float t = fmaf(z, p.inv_h, p.t_off);
+    t = fminf(fmaxf(t, 0.0f), p.tmax);
+    const float r = t + 12582912.0f;                 // rint(t) in the low bits
+    const int j = __float_as_int(r) - 0x4B400000;
+    const float x = t - (r - 12582912.0f);           // in [-1/2, 1/2]
+    const float4* c = reinterpret_cast<const float4*>(tabf + j * kPolyStride);
+    const float4 c0 = c[0], c1 = c[1], c2 = c[2];
+    float acc = fmaf(c2.w, x, c2.z);
+    acc = fmaf(acc, x, c2.y);
+    acc = fmaf(acc, x, c2.x);
+    acc = fmaf(acc, x, c1.w);
+    acc = fmaf(acc, x, c1.z);
+    acc = fmaf(acc, x, c1.y);
+    acc = fmaf(acc, x, c1.x);
+    acc = fmaf(acc, x, c0.w);
+    acc = fmaf(acc, x, c0.z);
+    acc = fmaf(acc, x, c0.y);
+    return fmaf(acc, x, c0.x);
 }
 
 // phi(z) as the reference writes it: all M centres (generic bandwidths).
@@ -153,7 +145,9 @@ struct StageCfg {
     static constexpr int FWD_ITEMS = NBX * NBY * kF;
     static constexpr int OBX = TW / 4;                   // output blocks
     static constexpr int OBY = TH / RB;
-    static_assert(OBX * OBY == NT, "one output block per thread");
+    static constexpr int NSPLIT = NT / (OBX * OBY);      // bwd filter split
+    static_assert(OBX * OBY * NSPLIT == NT && kF % NSPLIT == 0,
+                  "output blocks x filter split must cover the CTA");
     static_assert(TW % 4 == 0 && TH % RB == 0, "tile shape");
     static constexpr int SU = UR * US;
     static constexpr int SPHI = PH * PW;
@@ -164,7 +158,7 @@ struct StageCfg {
 };
 
 template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST>
-__global__ void __launch_bounds__(NT, 4) stage_kernel(const StageArgs p) {
+__global__ void __launch_bounds__(NT, 512 / NT) stage_kernel(const StageArgs p) {
     using C = StageCfg<MS, TH, TW, RF, RB, NT>;
     constexpr int R = C::R;
     extern __shared__ __align__(16) float smem[];
@@ -218,7 +212,8 @@ __global__ void __launch_bounds__(NT, 4) stage_kernel(const StageArgs p) {
     const bool fix_b = !bot_halo && (Y0 + TH + R > p.H);
     const bool need_fix = fix_l || fix_r || fix_t || fix_b;
 
-    const int obx = tid % C::OBX, oby = tid / C::OBX;
+    const int split = tid / (C::OBX * C::OBY);            // which filters of a group
+    const int obx = tid % C::OBX, oby = (tid / C::OBX) % C::OBY;
     const int ox0 = obx * 4, oy0 = oby * RB;
     float force[RB][4];
 #pragma unroll
@@ -287,10 +282,10 @@ __global__ void __launch_bounds__(NT, 4) stage_kernel(const StageArgs p) {
             for (int r = 0; r < RF; ++r) {
                 float4 o;
                 if (FAST) {
-                    o.x = rbf_fast(acc[r][0], tabf, p);
-                    o.y = rbf_fast(acc[r][1], tabf, p);
-                    o.z = rbf_fast(acc[r][2], tabf, p);
-                    o.w = rbf_fast(acc[r][3], tabf, p);
+                    o.x = rbf_poly(acc[r][0], tabf, p);
+                    o.y = rbf_poly(acc[r][1], tabf, p);
+                    o.z = rbf_poly(acc[r][2], tabf, p);
+                    o.w = rbf_poly(acc[r][3], tabf, p);
                 } else {
                     o.x = rbf_direct(acc[r][0], tabf, p);
                     o.y = rbf_direct(acc[r][1], tabf, p);
@@ -325,7 +320,7 @@ __global__ void __launch_bounds__(NT, 4) stage_kernel(const StageArgs p) {
 
         // ---- backward: force += corr(phi_i, k_i) -----------------------------
 #pragma unroll 1
-        for (int fi = 0; fi < kF; ++fi) {
+        for (int fi = split; fi < kF; fi += C::NSPLIT) {
             float k[C::KK];
             {
                 const float4* t4 = reinterpret_cast<const float4*>(tapg + fi * C::KP);
@@ -362,6 +357,28 @@ __global__ void __launch_bounds__(NT, 4) stage_kernel(const StageArgs p) {
                 }
             }
         }
+    }
+
+    // ---- sum the filter-split partial forces --------------------------------
+    if (C::NSPLIT > 1) {
+        __syncthreads();  // everyone is done reading sPhi
+        float* red = sPhi;
+        const int slot = (oby * C::OBX + obx) * RB * 4;
+        if (split > 0) {
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    red[(split - 1) * C::OBX * C::OBY * RB * 4 + slot + r * 4 + c] = force[r][c];
+        }
+        __syncthreads();
+        if (split > 0) return;
+        for (int s2 = 1; s2 < C::NSPLIT; ++s2)
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    force[r][c] += red[(s2 - 1) * C::OBX * C::OBY * RB * 4 + slot + r * 4 + c];
     }
 
     // ---- epilogue: u~ = u - force, prox, checks, store ----------------------

@@ -143,10 +143,21 @@ def test_edge_shapes(cuda, oracle, H, W, m):
     assert st["rel"] <= REL_TOL, st
 
 
-def test_generic_rbf_path_parity(cuda, oracle):
-    """bandwidth > spacing selects the direct all-centre RBF path."""
+@pytest.mark.parametrize("key", ["c1", "c2", "c5"])
+def test_rbf_polynomial_tables_accuracy(cuda, key):
+    """The per-interval degree-11 fits of every phi_i are exact to far below
+    fp32 resolution (checked in float64 at model creation)."""
+    dm = tn.device_model_for(synth.config_model(synth.CONFIGS[key]))
+    err, scale, ni = dm.rbf_fit
+    assert dm.fast_rbf and ni > 0
+    assert err <= 1e-9 * scale, dm.rbf_fit
+
+
+def test_direct_rbf_path_parity(cuda, oracle):
+    """A bandwidth so narrow that the polynomial table would not fit in
+    shared memory selects the direct all-centre RBF path."""
     model = synth.make_model(7, 8, 2, 63, seed=3)
-    model.rbf = tn.RbfGrid(63, 310.0, bandwidth=23.0)
+    model.rbf = tn.RbfGrid(63, 310.0, bandwidth=1.5)
     dm = tn.device_model_for(model)
     assert not dm.fast_rbf
     f = np.random.default_rng(5).uniform(1, 255, (70, 90)).astype(np.float32)
