@@ -82,10 +82,12 @@ int tnrd_model_destroy(tnrd_model* model);
 int tnrd_model_info(const tnrd_model* model, int* m, int* nk, int* T, int* M,
                     int* fast_rbf);
 /* Accuracy of the polynomial RBF tables built at creation: max |p - phi|
- * over every interval/filter/stage (fp32-rounded coefficients, float64
- * evaluation), the largest sum_j |w_ij|, and the interval count. */
+ * over every interval/filter/stage with float64 and with the fp32-rounded
+ * coefficients the kernel uses (both evaluated in float64), the largest
+ * sum_j |w_ij|, and the interval count (0 on the direct path). */
 int tnrd_model_rbf_fit(const tnrd_model* model, double* max_abs_err,
-                       double* max_sum_abs_w, int* intervals);
+                       double* max_abs_err_fp32, double* max_sum_abs_w,
+                       int* intervals);
 
 /* Reset a device status block (stream-ordered memset). */
 int tnrd_status_reset(uint32_t* d_status, void* stream);

@@ -47,6 +47,7 @@ SIGNATURES = {
     "tnrd_model_info": (_c_int, [_vp] + [ctypes.POINTER(_c_int)] * 5),
     "tnrd_model_rbf_fit": (_c_int, [_vp, ctypes.POINTER(_c_dbl),
                                     ctypes.POINTER(_c_dbl),
+                                    ctypes.POINTER(_c_dbl),
                                     ctypes.POINTER(_c_int)]),
     "tnrd_status_reset": (_c_int, [_vp, _vp]),
     "tnrd_status_decode": (_c_int, [ctypes.POINTER(_c_u32),

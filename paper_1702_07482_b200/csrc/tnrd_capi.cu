@@ -73,6 +73,7 @@ struct tnrd_model {
     double zlo = 0, h = 0;  // polynomial intervals: centre j at zlo + j h
     int ni = 0;             // number of intervals
     double fit_err = 0;     // max |p(z) - phi(z)| over all filters/stages
+    double fit_err32 = 0;   // same with the fp32 coefficients
     double fit_scale = 0;   // max sum_j |w_ij|
     std::vector<double> lam;
     float* d_taps = nullptr;  // T * nk_pad * kp
@@ -90,10 +91,11 @@ static double phi_exact(const double* w, int M, double mu0, double delta, double
 }
 
 // Degree-11 interpolant of phi on [zc - h/2, zc + h/2] at Chebyshev nodes,
-// as monomial coefficients in x = (z - zc)/h.  Returns the max abs error of
-// the fp32-rounded coefficients over 41 check points.
+// as monomial coefficients in x = (z - zc)/h.  Returns the max abs
+// interpolation error (float64 coefficients) over 41 check points and, in
+// *err32, the same with the fp32-rounded coefficients the kernel uses.
 static double fit_interval(const double* w, int M, double mu0, double delta, double gamma,
-                           double zc, double h, float* out) {
+                           double zc, double h, float* out, double* err32) {
     constexpr int N = kPolyDeg + 1;
     long double A[N][N + 1];
     for (int k = 0; k < N; ++k) {
@@ -114,14 +116,24 @@ static double fit_interval(const double* w, int M, double mu0, double delta, dou
             for (int k = c; k <= N; ++k) A[r][k] -= f * A[c][k];
         }
     }
-    for (int d = 0; d < N; ++d) out[d] = (float)(A[d][N] / A[d][d]);
-    double err = 0.0;
+    double c[N];
+    for (int d = 0; d < N; ++d) {
+        c[d] = (double)(A[d][N] / A[d][d]);
+        out[d] = (float)c[d];
+    }
+    double err = 0.0, e32 = 0.0;
     for (int k = 0; k <= 40; ++k) {
         const double x = -0.5 + k / 40.0;
-        double acc = 0.0;
-        for (int d = N - 1; d >= 0; --d) acc = acc * x + (double)out[d];
-        err = std::max(err, std::fabs(acc - phi_exact(w, M, mu0, delta, gamma, zc + x * h)));
+        double acc = 0.0, acc32 = 0.0;
+        for (int d = N - 1; d >= 0; --d) {
+            acc = acc * x + c[d];
+            acc32 = acc32 * x + (double)out[d];
+        }
+        const double ref = phi_exact(w, M, mu0, delta, gamma, zc + x * h);
+        err = std::max(err, std::fabs(acc - ref));
+        e32 = std::max(e32, std::fabs(acc32 - ref));
     }
+    *err32 = e32;
     return err;
 }
 
@@ -182,11 +194,14 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
                 double sw = 0.0;
                 for (int j = 0; j < M; ++j) sw += std::fabs(w[j]);
                 md->fit_scale = std::max(md->fit_scale, sw);
-                for (int q = 0; q < md->ni; ++q)
+                for (int q = 0; q < md->ni; ++q) {
+                    double e32 = 0.0;
                     md->fit_err = std::max(md->fit_err,
                                            fit_interval(w, M, mu0, delta, gamma,
                                                         md->zlo + q * md->h, md->h,
-                                                        tb + q * kPolyStride));
+                                                        tb + q * kPolyStride, &e32));
+                    md->fit_err32 = std::max(md->fit_err32, e32);
+                }
             } else {
                 for (int j = 0; j < M; ++j) tb[j] = (float)w[j];
             }
@@ -226,10 +241,12 @@ extern "C" int tnrd_model_destroy(tnrd_model* md) {
     return TNRD_OK;
 }
 
-extern "C" int tnrd_model_rbf_fit(const tnrd_model* md, double* max_abs_err, double* max_sum_abs_w,
+extern "C" int tnrd_model_rbf_fit(const tnrd_model* md, double* max_abs_err,
+                                  double* max_abs_err_fp32, double* max_sum_abs_w,
                                   int* intervals) {
     if (!md) return fail(TNRD_EINVAL, "model is NULL");
     if (max_abs_err) *max_abs_err = md->fit_err;
+    if (max_abs_err_fp32) *max_abs_err_fp32 = md->fit_err32;
     if (max_sum_abs_w) *max_sum_abs_w = md->fit_scale;
     if (intervals) *intervals = md->fast ? md->ni : 0;
     return TNRD_OK;

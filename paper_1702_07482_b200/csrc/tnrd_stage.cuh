@@ -40,6 +40,17 @@ constexpr float kFFloor = 1e-6f;  // speckle.py:21
 
 __host__ __device__ constexpr int round_up(int x, int a) { return (x + a - 1) / a * a; }
 
+// u-tile row stride: at least `need`, a multiple of 4 floats, and chosen so
+// that a step of `rows` rows shifts the bank by 4*nbx (mod 32 banks): the
+// float4 loads of consecutive forward blocks that straddle a block-row
+// boundary then hit disjoint banks.
+__host__ __device__ constexpr int padded_stride(int need, int rows, int nbx) {
+    int s = round_up(need, 4);
+    for (int k = 0; k < 8; ++k, s += 4)
+        if ((rows * s - 4 * nbx) % 32 == 0) return s;
+    return round_up(need, 4);
+}
+
 struct StageArgs {
     const float* u_in;
     const float* f;
@@ -136,7 +147,7 @@ struct StageCfg {
     static constexpr int PH = round_up(TH + 2 * R, RF);  // phi rows computed
     static constexpr int PW = round_up(TW + 2 * R, 4);   // phi cols computed (stride)
     static constexpr int UR = PH + 2 * R;                // u rows staged
-    static constexpr int US = PW + round_up(2 * R, 4);   // u row stride
+    static constexpr int US = padded_stride(PW + round_up(2 * R, 4), RF, PW / 4);  // u row stride
     static constexpr int NV = (4 + 2 * R + 3) / 4;       // float4 per row segment
     static constexpr int KK = MS * MS;
     static constexpr int KP = round_up(KK, 4);

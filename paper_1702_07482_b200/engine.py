@@ -119,11 +119,13 @@ class DeviceModel:
         _lib.check(L.tnrd_model_info(h, None, None, None, None,
                                      ctypes.byref(fast)))
         self.fast_rbf = bool(fast.value)
-        err, scale, ni = ctypes.c_double(0), ctypes.c_double(0), ctypes.c_int(0)
-        _lib.check(L.tnrd_model_rbf_fit(h, ctypes.byref(err), ctypes.byref(scale),
-                                        ctypes.byref(ni)))
-        # polynomial RBF table accuracy (max |p - phi|, max sum|w|, intervals)
-        self.rbf_fit = (err.value, scale.value, ni.value)
+        err, e32 = ctypes.c_double(0), ctypes.c_double(0)
+        scale, ni = ctypes.c_double(0), ctypes.c_int(0)
+        _lib.check(L.tnrd_model_rbf_fit(h, ctypes.byref(err), ctypes.byref(e32),
+                                        ctypes.byref(scale), ctypes.byref(ni)))
+        # polynomial RBF tables: (max |p - phi| float64 coeffs, fp32 coeffs,
+        # max sum|w|, intervals)
+        self.rbf_fit = (err.value, e32.value, scale.value, ni.value)
         self._plans = {}
         self._plan_lock = threading.Lock()
         self._status = {}

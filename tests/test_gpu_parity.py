@@ -148,9 +148,10 @@ def test_rbf_polynomial_tables_accuracy(cuda, key):
     """The per-interval degree-11 fits of every phi_i are exact to far below
     fp32 resolution (checked in float64 at model creation)."""
     dm = tn.device_model_for(synth.config_model(synth.CONFIGS[key]))
-    err, scale, ni = dm.rbf_fit
+    err, err32, scale, ni = dm.rbf_fit
     assert dm.fast_rbf and ni > 0
-    assert err <= 1e-9 * scale, dm.rbf_fit
+    assert err <= 1e-9 * scale, dm.rbf_fit      # interpolation itself
+    assert err32 <= 1e-7 * scale, dm.rbf_fit    # ~ fp32 resolution of phi
 
 
 def test_direct_rbf_path_parity(cuda, oracle):
