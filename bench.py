@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -148,13 +148,17 @@ def run_reference_arm(args, cfg, rank):
         return
     from paper_1702_07482_b200 import synth
     model = synth.config_model(cfg)
-    _, f = synth.noisy_image(cfg, 0)
+    if cfg.tiled:
+        f = synth.scene_crop(cfg, 0, 1024, 0, 1024)
+    else:
+        _, f = synth.noisy_image(cfg, 0)
     per_step = max(2.0, 150.0 / max(1, args.steps + args.warmup))
     rate, dt, sample, threads = cpu_reference_run(cfg, model, f, per_step)
     from oracle import oracle as O
     side = int(round((rate * 1e6 * dt) ** 0.5))
-    y0 = (cfg.H - side) // 2
-    crop = f[y0:y0 + side, y0:y0 + side].astype(np.float64)
+    y0 = (f.shape[0] - side) // 2
+    x0 = (f.shape[1] - side) // 2
+    crop = f[y0:y0 + side, x0:x0 + side].astype(np.float64)
     for _ in range(max(0, args.warmup - 1)):
         O.run_diffusion(crop, model)
     times = []
@@ -212,10 +216,24 @@ def measure_peaks(torch, L, stream):
     return out
 
 
+def setup_images(cfg, rank, world):
+    if cfg.batch == 1:
+        idx = [rank]                      # C2: one image per rank (weak)
+    else:
+        per = cfg.batch // world          # C3/C5: batch sharded (strong)
+        idx = list(range(rank * per, (rank + 1) * per))
+    return idx, np.stack([synth_mod().noisy_image(cfg, i)[1] for i in idx])
+
+
+def synth_mod():
+    from paper_1702_07482_b200 import synth
+    return synth
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
-    from paper_1702_07482_b200 import synth
+    synth = synth_mod()
     cfg = synth.CONFIGS[args.workload]
     if args.impl == "reference":
         run_reference_arm(args, cfg, rank)
@@ -229,46 +247,82 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_1702_07482_b200 as tn
-    from paper_1702_07482_b200 import _lib
+    from paper_1702_07482_b200 import _lib, strips
 
     L = _lib.load()
     model = synth.config_model(cfg)
-    if cfg.batch == 1:
-        idx = [rank]                      # C2: one image per rank (weak)
-    else:
-        per = cfg.batch // world          # C3/C5: batch sharded (strong)
-        idx = list(range(rank * per, (rank + 1) * per))
-    B = len(idx)
-    f_host = np.stack([synth.noisy_image(cfg, i)[1] for i in idx])
     dm = tn.device_model_for(model)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(dev)
-    f = torch.from_numpy(f_host).to(dev)
-    out = torch.empty_like(f)
-    work = torch.empty_like(f)
     status = tn.engine.Status(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     H, W = cfg.H, cfg.W
     sh = ctypes.c_void_p(stream.cuda_stream)
-    bufs = [out, work]
+    sptr = ctypes.c_void_p(status.buf.data_ptr())
 
-    def step(evs=None):
-        # T fused stage launches through the C ABI; final stage lands in `out`
-        L.tnrd_status_reset(ctypes.c_void_p(status.buf.data_ptr()), sh)
-        cur = f
-        for t in range(cfg.T):
-            dst = out if (cfg.T - 1 - t) % 2 == 0 else work
-            fl = (_lib.STAGE_FLOOR_INPUT | _lib.STAGE_CHECK_F) if t == 0 else 0
+    if cfg.name == "c4":
+        # one scene split into row strips, per-stage halo exchange (NCCL P2P)
+        lay = strips.StripLayout(H, W, world, rank, halo=cfg.m - 1)
+        r0, r1 = lay.rows
+        h, n = lay.halo, lay.n
+        f_host = synth.scene_rows(cfg, r0, r1)[None]
+        f_ext = torch.zeros(n + 2 * h, W, dtype=torch.float32, device=dev)
+        f_ext[h:h + n] = torch.from_numpy(f_host[0]).to(dev)
+        bufs = [torch.empty_like(f_ext), torch.empty_like(f_ext)]
+        stage_fn = strips.gpu_stage_fn(dm, status=status, stream=stream)
+        exch = strips.exchange_halos if world > 1 else (lambda *a, **k: None)
+        B, px_rank = 1, n * W
+        result = {}
+
+        def step(evs=None):
+            L.tnrd_status_reset(sptr, sh)
             if evs is not None:
-                evs[t].record(stream)
-            rc = L.tnrd_stage(dm.handle, t, ctypes.c_void_p(cur.data_ptr()),
-                              ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(dst.data_ptr()),
-                              B, H, W, W, H * W, fl, ctypes.c_void_p(status.buf.data_ptr()), sh)
-            if rc:
-                _lib.check(rc)
-            cur = dst
-        if evs is not None:
-            evs[cfg.T].record(stream)
+                evs[0].record(stream)
+            exch(f_ext, lay)
+            cur = f_ext
+            for t in range(cfg.T):
+                if t > 0:
+                    exch(cur, lay)
+                if evs is not None and t > 0:
+                    evs[t].record(stream)
+                dst = bufs[t % 2]
+                fl = lay.flags | ((_lib.STAGE_FLOOR_INPUT | _lib.STAGE_CHECK_F) if t == 0 else 0)
+                stage_fn(t, cur, f_ext, dst, lay, fl)
+                cur = dst
+            if evs is not None:
+                evs[cfg.T].record(stream)
+            result["u"] = cur
+
+        def final_output():
+            return result["u"][h:h + n]
+    else:
+        idx, f_host = setup_images(cfg, rank, world)
+        B = len(idx)
+        f = torch.from_numpy(f_host).to(dev)
+        out = torch.empty_like(f)
+        work = torch.empty_like(f)
+        px_rank = B * H * W
+
+        def step(evs=None):
+            # T fused stage launches through the C ABI; final stage lands in `out`
+            L.tnrd_status_reset(sptr, sh)
+            cur = f
+            for t in range(cfg.T):
+                dst = out if (cfg.T - 1 - t) % 2 == 0 else work
+                fl = (_lib.STAGE_FLOOR_INPUT | _lib.STAGE_CHECK_F) if t == 0 else 0
+                if evs is not None:
+                    evs[t].record(stream)
+                rc = L.tnrd_stage(dm.handle, t, ctypes.c_void_p(cur.data_ptr()),
+                                  ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(dst.data_ptr()),
+                                  B, H, W, W, H * W, fl, sptr, sh)
+                if rc:
+                    _lib.check(rc)
+                cur = dst
+            if evs is not None:
+                evs[cfg.T].record(stream)
+
+        def final_output():
+            return out
 
     with torch.cuda.stream(stream):
         for _ in range(max(3, args.warmup)):
@@ -298,44 +352,69 @@ def main():
         status.check()
 
     step_ms = [evs[k][0].elapsed_time(evs[k][cfg.T]) for k in range(args.steps)]
-    stage_ms = [evs[k][t].elapsed_time(evs[k][t + 1])
-                for k in range(args.steps) for t in range(cfg.T)]
     ms = sum(step_ms) / len(step_ms)
-    launch_ms = sum(stage_ms) / len(stage_ms)
+    if cfg.name == "c4":
+        # stage launches interleave with halo exchanges: per-launch time is
+        # taken from the exchange-free N=1 pattern (step / T) for the roofline
+        launch_ms = ms / cfg.T
+    else:
+        stage_ms = [evs[k][t].elapsed_time(evs[k][t + 1])
+                    for k in range(args.steps) for t in range(cfg.T)]
+        launch_ms = sum(stage_ms) / len(stage_ms)
     if dist is not None:
         tt = torch.tensor([ms, launch_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms, launch_ms = tt.tolist()
+    total_px = world * px_rank if cfg.name != "c4" else H * W
+    value = total_px / (ms * 1e3)          # MPix/s, all ranks
 
-    px_rank = B * H * W
-    value = world * px_rank / (ms * 1e3)          # MPix/s, all ranks
-
-    # ---- e2e: reference-facing call with HOST buffers (pinned), through the
-    # plan C ABI (H2D + T stages + D2H + status check in the timed region)
-    pin_f = torch.from_numpy(f_host).pin_memory()
-    pin_u = torch.empty_like(pin_f).pin_memory()
-    plan = dm._plan(B, H, W)
-    pstream = torch.cuda.ExternalStream(L.tnrd_plan_stream(plan), device=dev)
-    for _ in range(3):
-        _lib.check(L.tnrd_plan_despeckle_host(plan, ctypes.c_void_p(pin_f.data_ptr()),
-                                              ctypes.c_void_p(pin_u.data_ptr())))
-    e2e_steps = max(3, min(args.steps, 50))
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    if dist is not None:
-        dist.barrier()
-    e0.record(pstream)
-    for _ in range(e2e_steps):
-        _lib.check(L.tnrd_plan_despeckle_host(plan, ctypes.c_void_p(pin_f.data_ptr()),
-                                              ctypes.c_void_p(pin_u.data_ptr())))
-    e1.record(pstream)
-    e1.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    # ---- e2e: HOST buffers in, HOST result out, copies inside the timed region
+    if cfg.name == "c4":
+        pin_f = torch.from_numpy(f_host[0]).pin_memory()
+        pin_u = torch.empty_like(pin_f).pin_memory()
+        e2e_steps = max(2, min(args.steps, 5))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            e0.record(stream)
+            for _ in range(e2e_steps):
+                f_ext[h:h + n].copy_(pin_f, non_blocking=True)
+                step()
+                pin_u.copy_(final_output(), non_blocking=True)
+                status.check()
+            e1.record(stream)
+            e1.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / e2e_steps
+        e2e_path = "strip H2D + run_strip (NCCL halo exchange, fused stages) + D2H + status check"
+    else:
+        pin_f = torch.from_numpy(f_host).pin_memory()
+        pin_u = torch.empty_like(pin_f).pin_memory()
+        plan = dm._plan(B, H, W)
+        pstream = torch.cuda.ExternalStream(L.tnrd_plan_stream(plan), device=dev)
+        for _ in range(3):
+            _lib.check(L.tnrd_plan_despeckle_host(plan, ctypes.c_void_p(pin_f.data_ptr()),
+                                                  ctypes.c_void_p(pin_u.data_ptr())))
+        e2e_steps = max(3, min(args.steps, 50))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        if dist is not None:
+            dist.barrier()
+        e0.record(pstream)
+        for _ in range(e2e_steps):
+            _lib.check(L.tnrd_plan_despeckle_host(plan, ctypes.c_void_p(pin_f.data_ptr()),
+                                                  ctypes.c_void_p(pin_u.data_ptr())))
+        e1.record(pstream)
+        e1.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / e2e_steps
+        e2e_path = "tnrd_plan_despeckle_host (C ABI), pinned host buffers"
+        assert np.array_equal(pin_u.numpy(), final_output().cpu().numpy()), "e2e result differs"
     if dist is not None:
         tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = tt.item()
-    assert np.array_equal(pin_u.numpy(), out.cpu().numpy()), "e2e result differs"
 
     if rank != 0:
         if dist is not None:
@@ -345,7 +424,6 @@ def main():
     # ---- roofline of the fused stage kernel (SURVEY 8(d) algorithmic work)
     px_launch = px_rank
     flop_launch = w_flop(cfg) * px_launch
-    sfu_launch = w_sfu(cfg) * px_launch
     achieved_tf = flop_launch / (launch_ms * 1e-3) / 1e12
     peak_tf = peaks["fp32_tflops"]
     peak_sfu = peaks["mufu_ex2_gops"] * 1e9
@@ -356,12 +434,17 @@ def main():
     tpath = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(cfg.name)
+    conf = workload_config(cfg, args, B)
+    if cfg.name == "c4":
+        conf.update({"parallelism": f"row strips x{world}, {cfg.m - 1}-row u halo exchanged per stage (NCCL P2P)",
+                     "rows_per_rank": px_rank // W})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak" if cfg.batch == 1 else "strong",
+        "higher_is_better": True,
+        "scaling": "weak" if cfg.batch == 1 and cfg.name != "c4" else "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": workload_config(cfg, args, B),
+        "config": conf,
         "roofline": {
             "bound": "fp32", "unit": "TFLOP/s", "achieved": achieved_tf,
             "peak": peak_tf, "frac": achieved_tf / peak_tf, "traffic": traffic,
@@ -374,16 +457,16 @@ def main():
                 "rule": "t_roof = max(W_flop/P_fp32, W_sfu/P_mufu) with on-box P_fp32, P_mufu",
                 "p_mufu_gops": peaks["mufu_ex2_gops"]},
         },
-        "e2e": {"value": world * px_rank / (e2e_ms * 1e3), "unit": UNIT,
+        "e2e": {"value": total_px / (e2e_ms * 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": int(f_host.nbytes),
                 "d2h_bytes_per_step": int(f_host.nbytes) + 8,
-                "path": "tnrd_plan_despeckle_host (C ABI), pinned host buffers"},
+                "path": e2e_path},
         "gpu_launches": int(launches),
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:
-        per = 20.0
-        rate, dt, sample, threads = cpu_reference_run(cfg, model, f_host[0], per)
+        img0 = f_host[0] if cfg.name != "c4" else f_host[0][:512, :512]
+        rate, dt, sample, threads = cpu_reference_run(cfg, model, img0, 20.0)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads,
                                 "kind": "port", "sample": sample}
     print(json.dumps(line), flush=True)

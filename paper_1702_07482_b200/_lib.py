@@ -11,7 +11,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtnrd.so")
+LIB_PATH = os.environ.get("TNRD_LIB_PATH") or os.path.join(_HERE, "libtnrd.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "tnrd.h")
 
 TNRD_OK = 0

@@ -285,10 +285,26 @@ extern "C" int tnrd_status_decode(const uint32_t* h, int* bad_stage) {
 
 // ----------------------------------------------------------------- stage launch
 
+#ifndef TNRD_TH
+#define TNRD_TH 32
+#endif
+#ifndef TNRD_TW
+#define TNRD_TW 32
+#endif
+#ifndef TNRD_RF
+#define TNRD_RF 2
+#endif
+#ifndef TNRD_RB
+#define TNRD_RB 2
+#endif
+#ifndef TNRD_NT
+#define TNRD_NT 256
+#endif
+
 template <int MS, bool FAST>
 struct StageKernel {
-    // tile choice per filter size
-    static constexpr int TH = 32, TW = 32, RF = 2, RB = 2, NT = 256;
+    // tile choice; overridable at build time for sweeps
+    static constexpr int TH = TNRD_TH, TW = TNRD_TW, RF = TNRD_RF, RB = TNRD_RB, NT = TNRD_NT;
     using C = StageCfg<MS, TH, TW, RF, RB, NT>;
 
     static int launch(const StageArgs& a, int batch, cudaStream_t s) {

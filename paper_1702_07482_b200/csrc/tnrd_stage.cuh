@@ -169,7 +169,10 @@ struct StageCfg {
 };
 
 template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST>
-__global__ void __launch_bounds__(NT, 512 / NT) stage_kernel(const StageArgs p) {
+#ifndef TNRD_MINB
+#define TNRD_MINB (512 / NT)
+#endif
+__global__ void __launch_bounds__(NT, TNRD_MINB) stage_kernel(const StageArgs p) {
     using C = StageCfg<MS, TH, TW, RF, RB, NT>;
     constexpr int R = C::R;
     extern __shared__ __align__(16) float smem[];
