@@ -89,6 +89,12 @@ int tnrd_model_rbf_fit(const tnrd_model* model, double* max_abs_err,
                        double* max_abs_err_fp32, double* max_sum_abs_w,
                        int* intervals);
 
+/* Stage kernel selection (process-wide): 0 = auto (the kernel measured
+ * fastest on B200), 1 = CUDA-core kernel, 2 = tcgen05
+ * forward-GEMM kernel (error if the model is unsupported: m > 7 or RBF
+ * tables too large). */
+int tnrd_set_stage_kernel(int mode);
+
 /* Reset a device status block (stream-ordered memset). */
 int tnrd_status_reset(uint32_t* d_status, void* stream);
 /* Decode a HOST copy of the status block: returns TNRD_OK, TNRD_EINVAL (bad

@@ -49,6 +49,7 @@ SIGNATURES = {
                                     ctypes.POINTER(_c_dbl),
                                     ctypes.POINTER(_c_dbl),
                                     ctypes.POINTER(_c_int)]),
+    "tnrd_set_stage_kernel": (_c_int, [_c_int]),
     "tnrd_status_reset": (_c_int, [_vp, _vp]),
     "tnrd_status_decode": (_c_int, [ctypes.POINTER(_c_u32),
                                     ctypes.POINTER(_c_int)]),
@@ -97,6 +98,9 @@ def load():
             fn.restype = res
             fn.argtypes = args
         _lib = L
+        mode = os.environ.get("TNRD_STAGE_KERNEL")  # experiments: 0 auto, 1 cuda-core, 2 tcgen05
+        if mode:
+            L.tnrd_set_stage_kernel(int(mode))
     return _lib
 
 
@@ -121,6 +125,14 @@ def check(rc: int) -> None:
 
 def dptr(a) -> _dp:
     return a.ctypes.data_as(_dp)
+
+
+KERNEL_AUTO, KERNEL_CUDA_CORE, KERNEL_TENSOR_CORE = 0, 1, 2
+
+
+def set_stage_kernel(mode: int) -> None:
+    """0 auto (tcgen05 forward GEMM where supported), 1 CUDA-core, 2 tcgen05."""
+    check(load().tnrd_set_stage_kernel(int(mode)))
 
 
 def launch_count() -> int:

@@ -18,6 +18,7 @@
 
 #include "../../include/tnrd.h"
 #include "tnrd_stage.cuh"
+#include "tnrd_stage_tc.cuh"
 
 using namespace tnrd;
 
@@ -78,7 +79,31 @@ struct tnrd_model {
     std::vector<double> lam;
     float* d_taps = nullptr;  // T * nk_pad * kp
     float* d_tab = nullptr;   // T * nk_pad * tab_stride
+    // tensor-core forward GEMM operand (m in {3,5,7}): per stage
+    // [nk_pad/16 groups][m][ksteps][2 prec][2 kc][16][4]
+    float* d_bop = nullptr;
+    size_t bop_stage = 0;     // floats per stage
 };
+
+// 0 = auto (the faster kernel as measured on B200: currently
+// the CUDA-core kernel), 1 = CUDA-core only, 2 = tensor-core required
+static std::atomic<int> g_kernel_mode{0};
+
+extern "C" int tnrd_set_stage_kernel(int mode) {
+    if (mode < 0 || mode > 2) return fail(TNRD_EINVAL, "stage kernel mode must be 0, 1 or 2");
+    g_kernel_mode.store(mode);
+    return TNRD_OK;
+}
+
+// round-to-nearest (ties away) to tf32, as cvt.rna.tf32.f32
+static float tf32_rna_host(float x) {
+    uint32_t b;
+    std::memcpy(&b, &x, 4);
+    b = (b + 0x1000u) & 0xFFFFE000u;
+    float r;
+    std::memcpy(&r, &b, 4);
+    return r;
+}
 
 // phi(z) of one filter, as the reference evaluates it (influence.py:40-45)
 static double phi_exact(const double* w, int M, double mu0, double delta, double gamma, double z) {
@@ -166,7 +191,7 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
 
     auto* md = new tnrd_model();
     md->m = m; md->nk = nk; md->T = T; md->M = M; md->device = device;
-    md->nk_pad = round_up(nk, kF);
+    md->nk_pad = round_up(nk, tc::kG);  // zero filters beyond nk
     md->mu0 = mu0; md->delta = delta; md->gamma = gamma;
     md->lam.assign(lam, lam + T);
     md->kp = round_up(m * m, 4);
@@ -207,12 +232,48 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
             }
         }
     }
+    // forward GEMM operand for the tensor-core kernel (kf = rot180(k), split
+    // into tf32 hi + lo), see tnrd_stage_tc.cuh
+    std::vector<float> bop;
+    if (m <= 7) {
+        const int ks = (m + 7) / 8, G = md->nk_pad / tc::kG;
+        md->bop_stage = (size_t)G * m * ks * 2 * 2 * tc::kG * 4;
+        bop.assign(md->bop_stage * T, 0.0f);
+        for (int t = 0; t < T; ++t)
+            for (int g = 0; g < G; ++g)
+                for (int a = 0; a < m; ++a)
+                    for (int kk = 0; kk < ks; ++kk)
+                        for (int kc = 0; kc < 2; ++kc)
+                            for (int n = 0; n < tc::kG; ++n)
+                                for (int e = 0; e < 4; ++e) {
+                                    const int i = g * tc::kG + n, b = 8 * kk + 4 * kc + e;
+                                    float v = 0.0f;
+                                    if (i < nk && b < m)
+                                        v = (float)kernels[(((size_t)t * nk + i) * m + (m - 1 - a)) * m + (m - 1 - b)];
+                                    const float hi = tf32_rna_host(v);
+                                    const size_t base = (size_t)t * md->bop_stage +
+                                        ((((size_t)g * m + a) * ks + kk) * 2) * (2 * tc::kG * 4);
+                                    bop[base + (kc * tc::kG + n) * 4 + e] = hi;
+                                    bop[base + 2 * tc::kG * 4 + (kc * tc::kG + n) * 4 + e] =
+                                        tf32_rna_host(v - hi);
+                                }
+    }
     {
         DeviceGuard dg(device);
+        if (!bop.empty()) {
+            cudaError_t eb = cudaMalloc(&md->d_bop, bop.size() * sizeof(float));
+            if (eb == cudaSuccess)
+                eb = cudaMemcpy(md->d_bop, bop.data(), bop.size() * sizeof(float), cudaMemcpyHostToDevice);
+            if (eb != cudaSuccess) {
+                cudaFree(md->d_bop);
+                delete md;
+                return fail(TNRD_ECUDA, "tensor-core operand upload failed: %s", cudaGetErrorString(eb));
+            }
+        }
         cudaError_t e1 = cudaMalloc(&md->d_taps, ntap * sizeof(float));
         cudaError_t e2 = cudaMalloc(&md->d_tab, ntab * sizeof(float));
         if (e1 != cudaSuccess || e2 != cudaSuccess) {
-            cudaFree(md->d_taps); cudaFree(md->d_tab);
+            cudaFree(md->d_taps); cudaFree(md->d_tab); cudaFree(md->d_bop);
             delete md;
             return fail(TNRD_ECUDA, "cudaMalloc of model parameters failed: %s",
                         cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
@@ -220,7 +281,7 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
         cudaError_t e3 = cudaMemcpy(md->d_taps, taps.data(), ntap * sizeof(float), cudaMemcpyHostToDevice);
         cudaError_t e4 = cudaMemcpy(md->d_tab, tab.data(), ntab * sizeof(float), cudaMemcpyHostToDevice);
         if (e3 != cudaSuccess || e4 != cudaSuccess) {
-            cudaFree(md->d_taps); cudaFree(md->d_tab);
+            cudaFree(md->d_taps); cudaFree(md->d_tab); cudaFree(md->d_bop);
             delete md;
             return fail(TNRD_ECUDA, "parameter upload failed: %s",
                         cudaGetErrorString(e3 != cudaSuccess ? e3 : e4));
@@ -236,6 +297,7 @@ extern "C" int tnrd_model_destroy(tnrd_model* md) {
         DeviceGuard dg(md->device);
         cudaFree(md->d_taps);
         cudaFree(md->d_tab);
+        cudaFree(md->d_bop);
     }
     delete md;
     return TNRD_OK;
@@ -330,6 +392,54 @@ struct StageKernel {
     }
 };
 
+template <int MS>
+struct StageKernelTC {
+    using C = tc::TcCfg<MS>;
+    static bool fits(int tab_stride) { return C::smem_bytes(tab_stride) <= 227 * 1024; }
+    static int launch(const StageArgs& a, const float* bop, int batch, cudaStream_t s) {
+        static std::mutex mu;
+        static uint64_t attr_set = 0;
+        const size_t smem = C::smem_bytes(a.tab_stride);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        auto kern = tc::stage_kernel_tc<MS>;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (!(attr_set & (1ull << (dev & 63)))) {
+                CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              227 * 1024));
+                attr_set |= 1ull << (dev & 63);
+            }
+        }
+        dim3 grid((a.W + C::TW - 1) / C::TW, (a.H + C::TH - 1) / C::TH, batch);
+        kern<<<grid, tc::kNT, smem, s>>>(a, bop);
+        CUDA_TRY(cudaGetLastError());
+        g_launches.fetch_add(1);
+        return TNRD_OK;
+    }
+};
+
+static bool tc_supported(const tnrd_model* md) {
+    if (!md->fast || !md->d_bop) return false;
+    switch (md->m) {
+        case 3: return StageKernelTC<3>::fits(md->tab_stride);
+        case 5: return StageKernelTC<5>::fits(md->tab_stride);
+        case 7: return StageKernelTC<7>::fits(md->tab_stride);
+        default: return false;
+    }
+}
+
+static int dispatch_tc(const tnrd_model* md, int t, StageArgs a, int batch, cudaStream_t s) {
+    a.ngroups = md->nk_pad / tc::kG;
+    const float* bop = md->d_bop + (size_t)t * md->bop_stage;
+    switch (md->m) {
+        case 3: return StageKernelTC<3>::launch(a, bop, batch, s);
+        case 5: return StageKernelTC<5>::launch(a, bop, batch, s);
+        case 7: return StageKernelTC<7>::launch(a, bop, batch, s);
+        default: return fail(TNRD_EUNSUPPORTED, "no tensor-core stage kernel for m=%d", md->m);
+    }
+}
+
 template <bool FAST>
 static int dispatch_m(int m, const StageArgs& a, int batch, cudaStream_t s) {
     switch (m) {
@@ -362,7 +472,8 @@ static int launch_stage(const tnrd_model* md, int t, const float* u_in, const fl
     a.tab = md->d_tab + (size_t)t * md->nk_pad * md->tab_stride;
     a.ld = ld; a.img_stride = image_stride;
     a.H = H; a.W = W;
-    a.ngroups = md->nk_pad / kF;
+    a.ngroups = round_up(md->nk, kF) / kF;
+    a.nk = md->nk;
     a.tab_stride = md->tab_stride;
     const double lam = md->lam[t];
     const double aa = 1.0 + 2.0 * lam;
@@ -380,6 +491,9 @@ static int launch_stage(const tnrd_model* md, int t, const float* u_in, const fl
     a.flags = flags;
     a.stage = t;
     a.status = d_status;
+    const int mode = g_kernel_mode.load();
+    if (mode == 2 && tc_supported(md)) return dispatch_tc(md, t, a, batch, s);
+    if (mode == 2) return fail(TNRD_EUNSUPPORTED, "tensor-core stage kernel unavailable for this model");
     return md->fast ? dispatch_m<true>(md->m, a, batch, s) : dispatch_m<false>(md->m, a, batch, s);
 }
 

@@ -60,7 +60,8 @@ struct StageArgs {
     int64_t ld;          // elements between rows
     int64_t img_stride;  // elements between images
     int H, W;
-    int ngroups;         // nk_pad / kF
+    int ngroups;         // filter groups (of kF, or tc::kG on the tensor-core path)
+    int nk;              // real filters (padding filters are zero)
     int tab_stride;      // floats per filter in tab
     // prox (speckle.py:111-121): a = 1 + 2 lam
     float lam4;          // 4 lam

@@ -1,0 +1,448 @@
+// tnrd_stage_tc.cuh -- fused TNRD stage with the forward filter bank on the
+// 5th-generation tensor cores (tcgen05.mma kind::tf32, 3xTF32 split).
+//
+// Same stage operator as tnrd_stage.cuh (reference diffusion.py:184-194);
+// only the forward convolution z_i = conv2d(u, k_i) (imageops.py:53-72)
+// moves from FFMA to tcgen05:
+//
+//   * the 49-tap stencil is a GEMM D[points x 16 filters] = A[points x taps]
+//     B[taps x 16 filters] per filter group.  No im2col: for tap row a and
+//     point class o = x mod 4, the A rows of 8 consecutive class-o points of
+//     one image row are the overlapping 16-byte windows u[y+a][4k+o .. 4k+o+7]
+//     of a class-shifted copy of the u row, i.e. exactly a K-major
+//     SWIZZLE_NONE core matrix with rows 16 B apart, LBO = 16 B (the second
+//     K-chunk starts one window later) and SBO = the copy's row stride.  One
+//     M=128 MMA covers 16 image rows x 8 class-o points of the 32-column phi
+//     region; a 32 x 32 region = 2 bands x 4 classes = 8 MMA blocks.
+//   * 3xTF32: u = u_hi + u_lo, k = k_hi + k_lo (hi = cvt.rna.tf32), D +=
+//     hi*hi + lo*hi + hi*lo with fp32 accumulation in TMEM (~2^-21 relative,
+//     single-pass TF32 fails the 1e-4 bar, 3xTF32 passes).
+//   * accumulators live in TMEM (2 x 128 columns, double-buffered by filter
+//     group so the tensor core computes group g+1 while the CUDA cores run
+//     the RBF + backward pass of group g); commit -> mbarrier -> tcgen05.ld.
+//   * RBF, phi mirror fix-up, backward correlation and the prox epilogue are
+//     the CUDA-core code of tnrd_stage.cuh.
+#pragma once
+#include "tnrd_stage.cuh"
+
+namespace tnrd {
+namespace tc {
+
+constexpr int kG = 16;           // filters per group (MMA N)
+constexpr int kPW = 32;          // phi-region width (4 classes x 8 points)
+constexpr int kPH = 32;          // phi-region height (2 bands of 16 rows)
+constexpr int kBlocks = 8;       // 2 bands x 4 classes, M = 128 each
+constexpr int kSPW = 36;         // sPhi row stride (floats)
+constexpr int kNT = 384;         // 12 warps = 3 warpgroups
+constexpr int kNSPLIT = 4;       // backward filter split (4 filters each)
+constexpr int kTmemCols = 256;   // 2 buffers x 8 blocks x 16 columns
+
+// instruction descriptor: kind::tf32, D f32, A/B tf32 K-major, M=128, N=16
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kG >> 3) << 17) |
+                            ((uint32_t)(128 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// SWIZZLE_NONE, K-major shared-memory matrix descriptor (sm_100 version 1)
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Host-prepared per-stage operand for the forward GEMM (built by
+// tnrd_model_create): for group g, ksteps kk (b = 8kk .. 8kk+7), tap row a,
+// precision p (0 hi, 1 lo): [kc (2)][n (16)][4 floats] = kf_n[a][8kk+4kc+..]
+// with kf = rot180(k) the correlation form of the true convolution.
+template <int MS>
+struct TcCfg {
+    static constexpr int R = MS / 2;
+    static constexpr int KSTEPS = (MS + 7) / 8;           // K = 8 per MMA
+    static constexpr int TH = (MS == 9) ? 24 : 26;        // output tile
+    static constexpr int TW = (MS == 9) ? 24 : (MS == 7 ? 26 : 28);
+    static constexpr int RB = 2;
+    static constexpr int OBX = (TW + 3) / 4;
+    static constexpr int OBY = TH / RB;
+    static constexpr int ITEMS = OBX * OBY * kNSPLIT;
+    static_assert(ITEMS <= kNT, "backward items must fit the CTA");
+    static_assert(TH + 2 * R <= kPH && TW + 2 * R <= kPW, "tile + halo must fit the phi region");
+    static_assert(4 * OBX + 2 * R <= kSPW, "backward reads past the phi row stride");
+    static constexpr int UR = kPH + 2 * R;                // u rows
+    static constexpr int CW = 32 + 8 * KSTEPS - 4;        // class-copy width (floats)
+    static constexpr int CS = round_up(CW, 4);            // class-copy row stride
+    static constexpr int COPY = UR * CS;                  // floats per class copy
+    static constexpr int BOP = 2 * kG * 4;                // floats per (a, kk, p) B operand
+    static constexpr int BGROUP = MS * KSTEPS * 2 * BOP;  // floats per group
+    static constexpr int KP = round_up(MS * MS, 4);
+    static constexpr int SPHI = kPH * kSPW;
+    // shared layout (floats)
+    static constexpr int OFF_COPY = 0;                              // [4 classes][2 prec][COPY]
+    static constexpr int OFF_B = OFF_COPY + 8 * COPY;               // [2 buf][BGROUP]
+    static constexpr int OFF_TAP = OFF_B + 2 * BGROUP;              // [2 buf][kG][KP]
+    static constexpr int OFF_PHI = OFF_TAP + 2 * kG * KP;           // [kG][SPHI]
+    static constexpr int OFF_TAB = OFF_PHI + kG * SPHI;             // [kG][tab_stride]
+    static size_t smem_bytes(int tab_stride) {
+        return sizeof(float) * (size_t)(OFF_TAB + kG * tab_stride) + 64;  // + barriers
+    }
+};
+
+template <int MS>
+__global__ void __launch_bounds__(kNT, 1) stage_kernel_tc(const StageArgs p, const float* __restrict__ bop) {
+    using C = TcCfg<MS>;
+    constexpr int R = C::R;
+    extern __shared__ __align__(128) float smem[];
+    float* sCopy = smem + C::OFF_COPY;
+    float* sB = smem + C::OFF_B;
+    float* sTap = smem + C::OFF_TAP;
+    float* sPhi = smem + C::OFF_PHI;
+    float* sTab = smem + C::OFF_TAB;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sTab + kG * p.tab_stride);  // [2] mma done
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int img = blockIdx.z;
+    const int Y0 = blockIdx.y * C::TH;
+    const int X0 = blockIdx.x * C::TW;
+    const float* __restrict__ uin = p.u_in + (int64_t)img * p.img_stride;
+    const float* __restrict__ fin = p.f + (int64_t)img * p.img_stride;
+    float* __restrict__ uout = p.u_out + (int64_t)img * p.img_stride;
+    const bool top_halo = p.flags & 0x2u;
+    const bool bot_halo = p.flags & 0x4u;
+    const int ngroups = p.ngroups;  // of kG filters
+
+    auto prefetch_b = [&](int g, int buf) {  // forward GEMM operand of group g
+        const float* gb = bop + (size_t)g * C::BGROUP;
+        float* sb = sB + buf * C::BGROUP;
+        for (int i = tid; i < C::BGROUP / 4; i += kNT) cp_async16(sb + 4 * i, gb + 4 * i);
+    };
+    auto prefetch_taps = [&](int g, int buf) {  // backward taps of group g
+        const float* gt = p.taps + (size_t)g * kG * C::KP;
+        float* st = sTap + buf * kG * C::KP;
+        for (int i = tid; i < kG * C::KP / 4; i += kNT) cp_async16(st + 4 * i, gt + 4 * i);
+    };
+    auto prefetch_tab = [&](int g) {
+        const float* gb = p.tab + (size_t)g * kG * p.tab_stride;
+        for (int i = tid; i < kG * p.tab_stride / 4; i += kNT) cp_async16(sTab + 4 * i, gb + 4 * i);
+    };
+
+    // ---- setup: barriers, TMEM, operands of group 0 -------------------------
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    prefetch_b(0, 0);
+    if (ngroups > 1) prefetch_b(1, 1);
+    prefetch_taps(0, 0);
+    prefetch_tab(0);
+    cp_async_commit();
+
+    // u region (2r halo), staged in sPhi (free until the first RBF phase)
+    constexpr int UW = C::CW + 3;  // u_reg columns needed by the class copies
+    float* sU = sPhi;
+    {
+        const bool floor_in = p.flags & 0x1u;
+        for (int i = tid; i < C::UR * UW; i += kNT) {
+            const int uy = i / UW, ux = i - uy * UW;
+            int Y = Y0 - 2 * R + uy;
+            const int X = mirror_clamp(X0 - 2 * R + ux, p.W);
+            if (Y < 0) Y = top_halo ? max(Y, -2 * R) : mirror_clamp(Y, p.H);
+            else if (Y >= p.H) Y = bot_halo ? min(Y, p.H - 1 + 2 * R) : mirror_clamp(Y, p.H);
+            float v = __ldg(uin + (int64_t)Y * p.ld + X);
+            if (floor_in) v = fmaxf(v, kFFloor);
+            sU[i] = v;
+        }
+    }
+    __syncthreads();
+    // class copies: copy[o][prec][ur][j] = hi/lo(u_reg[ur][j + o])
+    for (int i = tid; i < 4 * C::UR * C::CS; i += kNT) {
+        const int o = i / (C::UR * C::CS);
+        const int rem = i - o * (C::UR * C::CS);
+        const int ur = rem / C::CS, j = rem - ur * C::CS;
+        const float u = (j < C::CW) ? sU[ur * UW + j + o] : 0.0f;
+        const float hi = tf32_rna(u);
+        sCopy[(o * 2 + 0) * C::COPY + rem] = hi;
+        sCopy[(o * 2 + 1) * C::COPY + rem] = tf32_rna(u - hi);  // |u - hi - lo| <= 2^-22 |u|
+    }
+    cp_async_wait_all();
+    fence_async_smem();
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+
+    // one elected thread issues the 8 blocks x taps x 3 passes of group g
+    auto issue_group = [&](int g) {
+        const int buf = g & 1;
+        const float* sb = sB + buf * C::BGROUP;
+        for (int blk = 0; blk < kBlocks; ++blk) {
+            const int band = blk >> 2, o = blk & 3;
+            const uint32_t d = tmem + (uint32_t)(buf * 128 + blk * kG);
+            int first = 1;
+            for (int a = 0; a < MS; ++a) {
+                for (int kk = 0; kk < C::KSTEPS; ++kk) {
+                    const uint32_t arow = (uint32_t)((16 * band + a) * C::CS + 8 * kk) * 4u;
+                    const uint64_t ahi = make_desc(smem_u32(sCopy + (o * 2 + 0) * C::COPY) + arow, 16, C::CS * 4);
+                    const uint64_t alo = make_desc(smem_u32(sCopy + (o * 2 + 1) * C::COPY) + arow, 16, C::CS * 4);
+                    const float* bb = sb + ((a * C::KSTEPS + kk) * 2) * C::BOP;
+                    const uint64_t bhi = make_desc(smem_u32(bb), kG * 16, 128);
+                    const uint64_t blo = make_desc(smem_u32(bb + C::BOP), kG * 16, 128);
+                    mma_tf32(d, ahi, bhi, first ? 0u : 1u);
+                    mma_tf32(d, alo, bhi, 1u);
+                    mma_tf32(d, ahi, blo, 1u);
+                    first = 0;
+                }
+            }
+        }
+        mma_commit(&bars[buf]);
+    };
+
+    if (tid == 0) issue_group(0);
+
+    // tile touches a mirrored image edge? (phi halo fix-up needed)
+    const bool fix_l = X0 - R < 0;
+    const bool fix_r = X0 + C::TW + R > p.W;
+    const bool fix_t = !top_halo && (Y0 - R < 0);
+    const bool fix_b = !bot_halo && (Y0 + C::TH + R > p.H);
+    const bool need_fix = fix_l || fix_r || fix_t || fix_b;
+
+    // backward item of this thread
+    const bool has_item = tid < C::ITEMS;
+    const int obx = tid % C::OBX, oby = (tid / C::OBX) % C::OBY, split = tid / (C::OBX * C::OBY);
+    const int ox0 = obx * 4, oy0 = oby * C::RB;
+    float force[C::RB][4];
+#pragma unroll
+    for (int r = 0; r < C::RB; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) force[r][c] = 0.0f;
+
+    const int wg = warp >> 2, q = warp & 3;
+    for (int g = 0; g < ngroups; ++g) {
+        const int buf = g & 1;
+        // ---- z of group g ready in TMEM --------------------------------------
+        mbar_wait(&bars[buf], (g >> 1) & 1);
+        fence_after();
+        // ---- RBF: TMEM -> phi -> sPhi ----------------------------------------
+        for (int blk = wg; blk < kBlocks; blk += 3) {
+            float z[kG];
+            tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * 128 + blk * kG), z);
+            const int row = 32 * q + lane;
+            const int py = 16 * (blk >> 2) + (row >> 3);
+            const int px = 4 * (row & 7) + (blk & 3);
+#pragma unroll
+            for (int j = 0; j < kG; ++j) {
+                if (g * kG + j < p.nk)
+                    sPhi[j * C::SPHI + py * kSPW + px] = rbf_poly(z[j], sTab + j * p.tab_stride, p);
+            }
+        }
+        fence_before();
+        __syncthreads();  // sPhi complete; TMEM buffer `buf` drained; B[buf] free
+        // tables + taps of group g+1 and the GEMM operand of group g+2 stream
+        // in during the backward pass
+        if (g + 2 < ngroups) prefetch_b(g + 2, buf);
+        if (g + 1 < ngroups) {
+            prefetch_taps(g + 1, buf ^ 1);
+            prefetch_tab(g + 1);
+        }
+        cp_async_commit();
+        if (tid == 0 && g + 1 < ngroups) {
+            fence_after();
+            issue_group(g + 1);  // B[(g+1)&1] landed at the previous barrier
+        }
+        // ---- phi halo outside the image = mirror of in-image phi -------------
+        if (need_fix) {
+            for (int i = tid; i < kG * C::SPHI; i += kNT) {
+                const int j = i / C::SPHI;
+                const int rem = i - j * C::SPHI;
+                const int py = rem / kSPW, px = rem - py * kSPW;
+                if (px >= kPW) continue;
+                const int Y = Y0 - R + py, X = X0 - R + px;
+                int sy = Y, sx = X;
+                if (X < 0 && X >= -R) sx = -1 - X;
+                else if (X >= p.W && X < p.W + R) sx = 2 * p.W - 1 - X;
+                if (!top_halo && Y < 0 && Y >= -R) sy = -1 - Y;
+                else if (!bot_halo && Y >= p.H && Y < p.H + R) sy = 2 * p.H - 1 - Y;
+                if (sy != Y || sx != X) {
+                    const int spy = sy - (Y0 - R), spx = sx - (X0 - R);
+                    sPhi[j * C::SPHI + py * kSPW + px] = sPhi[j * C::SPHI + spy * kSPW + spx];
+                }
+            }
+            __syncthreads();
+        }
+        // ---- backward: force += corr(phi_j, k_j), 4 filters per item ---------
+        if (has_item) {
+            const float* tapg = sTap + buf * kG * C::KP;
+#pragma unroll 1
+            for (int jj = 0; jj < kG / kNSPLIT; ++jj) {
+                const int j = split * (kG / kNSPLIT) + jj;
+                if (g * kG + j >= p.nk) break;
+                float k[MS * MS];
+                {
+                    const float4* t4 = reinterpret_cast<const float4*>(tapg + j * C::KP);
+#pragma unroll
+                    for (int qq = 0; qq < C::KP / 4; ++qq) {
+                        const float4 v = t4[qq];
+                        if (4 * qq + 0 < MS * MS) k[4 * qq + 0] = v.x;
+                        if (4 * qq + 1 < MS * MS) k[4 * qq + 1] = v.y;
+                        if (4 * qq + 2 < MS * MS) k[4 * qq + 2] = v.z;
+                        if (4 * qq + 3 < MS * MS) k[4 * qq + 3] = v.w;
+                    }
+                }
+                constexpr int NV = (4 + 2 * R + 3) / 4;
+                const float* ph = sPhi + j * C::SPHI;
+#pragma unroll
+                for (int rr = 0; rr < C::RB + 2 * R; ++rr) {
+                    float v[4 * NV];
+                    const float4* src = reinterpret_cast<const float4*>(ph + (oy0 + rr) * kSPW + ox0);
+#pragma unroll
+                    for (int qq = 0; qq < NV; ++qq) {
+                        const float4 t = src[qq];
+                        v[4 * qq] = t.x; v[4 * qq + 1] = t.y; v[4 * qq + 2] = t.z; v[4 * qq + 3] = t.w;
+                    }
+#pragma unroll
+                    for (int a = 0; a < MS; ++a) {
+                        const int ro = rr - a;
+                        if (ro >= 0 && ro < C::RB) {
+#pragma unroll
+                            for (int b = 0; b < MS; ++b) {
+                                const float kk = k[a * MS + b];
+#pragma unroll
+                                for (int c = 0; c < 4; ++c) force[ro][c] = fmaf(kk, v[c + b], force[ro][c]);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        cp_async_wait_all();
+        fence_async_smem();
+        __syncthreads();  // bwd done with sPhi/taps; next tables + B landed
+    }
+
+    // ---- release TMEM --------------------------------------------------------
+    fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
+    }
+
+    // ---- reduce the filter splits, epilogue ------------------------------------
+    float* red = sPhi;
+    const int slot = (oby * C::OBX + obx) * C::RB * 4;
+    if (has_item && split > 0) {
+#pragma unroll
+        for (int r = 0; r < C::RB; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                red[(split - 1) * C::OBX * C::OBY * C::RB * 4 + slot + r * 4 + c] = force[r][c];
+    }
+    __syncthreads();
+    if (!has_item || split > 0) return;
+    for (int s2 = 1; s2 < kNSPLIT; ++s2)
+#pragma unroll
+        for (int r = 0; r < C::RB; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                force[r][c] += red[(s2 - 1) * C::OBX * C::OBY * C::RB * 4 + slot + r * 4 + c];
+
+    const bool out_force = p.flags & 0x8u;
+    const bool check_f = p.flags & 0x10u;
+    bool bad = false;
+    uint32_t fbits = 0;
+#pragma unroll
+    for (int r = 0; r < C::RB; ++r) {
+        const int oy = oy0 + r, Y = Y0 + oy;
+        if (Y >= p.H) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int ox = ox0 + c, X = X0 + ox;
+            if (ox >= C::TW || X >= p.W) continue;
+            float res;
+            if (out_force) {
+                res = force[r][c];
+            } else {
+                float u = __ldg(uin + (int64_t)Y * p.ld + X);  // exact u (copies are split)
+                if (p.flags & 0x1u) u = fmaxf(u, kFFloor);
+                const float fv = __ldg(fin + (int64_t)Y * p.ld + X);
+                if (check_f) {
+                    if (!isfinite(fv)) fbits |= 0x1u;
+                    else if (fv < 0.0f) fbits |= 0x2u;
+                }
+                const float ff = fmaxf(fv, kFFloor);
+                const float ut = u - force[r][c];
+                const float fl2 = ff * ff;
+                const float root = sqrtf(fmaf(ut, ut, p.c8 * fl2));
+                res = ut >= 0.0f ? (ut + root) * p.inv2a : (p.lam4 * fl2) / (root - ut);
+            }
+            if (!isfinite(res)) bad = true;
+            uout[(int64_t)Y * p.ld + X] = res;
+        }
+    }
+    if (bad) atomicMin(p.status, (uint32_t)p.stage);
+    if (fbits) atomicAnd(p.status + 1, ~fbits);
+}
+
+}  // namespace tc
+}  // namespace tnrd

@@ -1,0 +1,87 @@
+"""The tensor-core stage kernel (tcgen05 3xTF32 forward GEMM) must meet the
+same parity bar as the CUDA-core kernel: golden vectors, full C1/C2 images,
+ragged shapes, strip mode, batch launches."""
+import numpy as np
+import pytest
+
+from conftest import golden_model, golden_names, load_golden, parity_stats
+
+import paper_1702_07482_b200 as tn
+from paper_1702_07482_b200 import _lib, synth
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-4
+PSNR_TOL = 0.01
+
+
+@pytest.fixture
+def tc_mode(cuda):
+    _lib.set_stage_kernel(_lib.KERNEL_TENSOR_CORE)
+    yield
+    _lib.set_stage_kernel(_lib.KERNEL_AUTO)
+
+
+def _tc_ok(m):
+    return m in (3, 5, 7)
+
+
+@pytest.mark.parametrize("name", golden_names(full_only=True))
+def test_tc_golden_cases(tc_mode, name):
+    g = load_golden(name)
+    if not _tc_ok(int(g["m"])):
+        pytest.skip("no tensor-core kernel for this m")
+    model = golden_model(g)
+    if not tn.device_model_for(model).fast_rbf:
+        pytest.skip("direct-RBF model")
+    u, _ = tn.run_diffusion(g["f"], model)
+    st = parity_stats(u, g["u"], g.get("clean"))
+    assert st["rel"] <= REL_TOL and st["abs_degenerate"] <= 1e-9, st
+
+
+@pytest.mark.parametrize("key", ["c1", "c2"])
+def test_tc_full_configs(tc_mode, oracle, key):
+    cfg = synth.CONFIGS[key]
+    clean, f = synth.noisy_image(cfg, 0)
+    model = synth.config_model(cfg)
+    u, _ = tn.run_diffusion(f, model)
+    ref = oracle.run_diffusion(f.astype(np.float64), model)
+    st = parity_stats(u, ref, clean)
+    assert st["rel"] <= REL_TOL and st["dpsnr"] <= PSNR_TOL, st
+
+
+@pytest.mark.parametrize("H,W,m", [(3, 200, 7), (200, 3, 7), (33, 65, 3), (64, 31, 5),
+                                   (97, 130, 7), (27, 27, 5)])
+def test_tc_edge_shapes(tc_mode, oracle, H, W, m):
+    model = synth.make_model(m, 20, 2, 63, seed=H * 1000 + W)
+    f = np.random.default_rng(H + W).uniform(0, 300, (H, W)).astype(np.float32)
+    u, _ = tn.run_diffusion(f, model)
+    ref = oracle.run_diffusion(f.astype(np.float64), model)
+    assert parity_stats(u, ref)["rel"] <= REL_TOL
+
+
+def test_tc_matches_cuda_core_kernel(cuda):
+    torch = cuda
+    cfg = synth.CONFIGS["c3"]
+    model = synth.config_model(cfg)
+    f = torch.from_numpy(np.stack([synth.noisy_image(cfg, i)[1] for i in range(3)])).cuda()
+    _lib.set_stage_kernel(_lib.KERNEL_CUDA_CORE)
+    try:
+        a = tn.run_diffusion_batch(f, model).cpu().numpy()
+        _lib.set_stage_kernel(_lib.KERNEL_TENSOR_CORE)
+        b = tn.run_diffusion_batch(f, model).cpu().numpy()
+    finally:
+        _lib.set_stage_kernel(_lib.KERNEL_AUTO)
+    assert np.max(np.abs(a - b) / a) < 2e-5
+
+
+def test_tc_strips_bit_identical(tc_mode):
+    from test_gpu_strips import lockstep_strips
+    import torch
+    model = synth.make_model(7, 32, 3, 63, seed=5)
+    H, W = 180, 75
+    f = torch.from_numpy(np.random.default_rng(1).uniform(0, 300, (H, W)).astype(np.float32)).cuda()
+    dm = tn.device_model_for(model)
+    whole = dm.despeckle(f)
+    got = lockstep_strips(dm, f, 3, model.num_stages)
+    assert torch.equal(got, whole)
