@@ -73,6 +73,7 @@ struct tnrd_model {
     double mu0 = 0, delta = 0, gamma = 0;
     double zlo = 0, h = 0;  // polynomial intervals: centre j at zlo + j h
     int ni = 0;             // number of intervals
+    int nip = 0;            // intervals rounded to 4 (coefficient-plane stride)
     double fit_err = 0;     // max |p(z) - phi(z)| over all filters/stages
     double fit_err32 = 0;   // same with the fp32 coefficients
     double fit_scale = 0;   // max sum_j |w_ij|
@@ -115,12 +116,13 @@ static double phi_exact(const double* w, int M, double mu0, double delta, double
     return s;
 }
 
-// Degree-11 interpolant of phi on [zc - h/2, zc + h/2] at Chebyshev nodes,
-// as monomial coefficients in x = (z - zc)/h.  Returns the max abs
-// interpolation error (float64 coefficients) over 41 check points and, in
-// *err32, the same with the fp32-rounded coefficients the kernel uses.
+// Degree-7 interpolant of phi on [zc - h/2, zc + h/2] at Chebyshev nodes,
+// as monomial coefficients in x = (z - zc)/h, written to out[d * ostride].
+// Returns the max abs interpolation error (float64 coefficients) over 41
+// check points and, in *err32, the same with the fp32-rounded coefficients
+// the kernel uses.
 static double fit_interval(const double* w, int M, double mu0, double delta, double gamma,
-                           double zc, double h, float* out, double* err32) {
+                           double zc, double h, float* out, int ostride, double* err32) {
     constexpr int N = kPolyDeg + 1;
     long double A[N][N + 1];
     for (int k = 0; k < N; ++k) {
@@ -142,9 +144,11 @@ static double fit_interval(const double* w, int M, double mu0, double delta, dou
         }
     }
     double c[N];
+    float c32[N];
     for (int d = 0; d < N; ++d) {
         c[d] = (double)(A[d][N] / A[d][d]);
-        out[d] = (float)c[d];
+        c32[d] = (float)c[d];
+        out[(size_t)d * ostride] = c32[d];
     }
     double err = 0.0, e32 = 0.0;
     for (int k = 0; k <= 40; ++k) {
@@ -152,7 +156,7 @@ static double fit_interval(const double* w, int M, double mu0, double delta, dou
         double acc = 0.0, acc32 = 0.0;
         for (int d = N - 1; d >= 0; --d) {
             acc = acc * x + c[d];
-            acc32 = acc32 * x + (double)out[d];
+            acc32 = acc32 * x + (double)c32[d];
         }
         const double ref = phi_exact(w, M, mu0, delta, gamma, zc + x * h);
         err = std::max(err, std::fabs(acc - ref));
@@ -198,12 +202,13 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
     // piecewise-polynomial RBF: intervals of width h = min(delta, gamma)
     // (one Gaussian std or less, so degree 11 reaches ~1e-11 of sum|w|) over
     // [mu_0 - 7 gamma, mu_{M-1} + 7 gamma]; beyond that phi < 3e-11 sum|w|.
-    md->h = std::min(delta, gamma);
+    md->h = std::min(delta, gamma) / kPolySub;
     md->zlo = mu0 - 7.0 * gamma;
     const double zhi = mu0 + (M - 1) * delta + 7.0 * gamma;
     md->ni = (int)std::ceil((zhi - md->zlo) / md->h) + 1;
-    md->fast = (size_t)md->ni * kPolyStride * kF <= 16384;  // <= 64 KB per group buffer
-    md->tab_stride = md->fast ? md->ni * kPolyStride : round_up(M, 4);
+    md->nip = round_up(md->ni, 4);
+    md->fast = (size_t)md->nip * kPolyN * kF <= 16384;  // <= 64 KB per group buffer
+    md->tab_stride = md->fast ? md->nip * kPolyN : round_up(M, 4);
 
     const size_t ntap = (size_t)T * md->nk_pad * md->kp;
     const size_t ntab = (size_t)T * md->nk_pad * md->tab_stride;
@@ -224,7 +229,7 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
                     md->fit_err = std::max(md->fit_err,
                                            fit_interval(w, M, mu0, delta, gamma,
                                                         md->zlo + q * md->h, md->h,
-                                                        tb + q * kPolyStride, &e32));
+                                                        tb + q, md->nip, &e32));
                     md->fit_err32 = std::max(md->fit_err32, e32);
                 }
             } else {
@@ -482,6 +487,7 @@ static int launch_stage(const tnrd_model* md, int t, const float* u_in, const fl
     a.inv2a = (float)(1.0 / (2.0 * aa));
     const double L2E = 1.4426950408889634;
     a.inv_h = (float)(1.0 / md->h);
+    a.tab_ni = md->nip;
     a.t_off = (float)(-md->zlo / md->h);
     a.tmax = (float)(md->ni - 1);
     a.delta = (float)md->delta;

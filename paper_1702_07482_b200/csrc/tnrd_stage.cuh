@@ -34,8 +34,9 @@
 namespace tnrd {
 
 constexpr int kF = 4;          // filters per group
-constexpr int kPolyDeg = 11;   // RBF interpolant degree per interval
-constexpr int kPolyStride = 12;  // floats per interval (degree + 1)
+constexpr int kPolyDeg = 7;    // RBF interpolant degree per interval
+constexpr int kPolyN = kPolyDeg + 1;  // coefficients per interval
+constexpr int kPolySub = 2;    // intervals per min(delta, gamma)
 constexpr float kFFloor = 1e-6f;  // speckle.py:21
 
 __host__ __device__ constexpr int round_up(int x, int a) { return (x + a - 1) / a * a; }
@@ -67,8 +68,10 @@ struct StageArgs {
     float lam4;          // 4 lam
     float c8;            // 8 a lam
     float inv2a;         // 1 / (2a)
-    // RBF: polynomial table (default) -- t = z / h + t_off, clamp [0, tmax]
+    // RBF: polynomial table (default) -- t = z / h + t_off, clamp [0, tmax];
+    // coefficient d of interval j at tab[d * tab_ni + j]
     float inv_h;
+    int tab_ni;
     float t_off;
     float tmax;
     // RBF: direct all-centre sum (fallback for very large tables)
@@ -85,6 +88,21 @@ __device__ __forceinline__ float ex2f(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+// 128-bit shared load that the compiler may not narrow (a narrowed LDS.64
+// tail breaks the 8-lane conflict-free phase pattern of the row loads).
+// The "memory" clobber keeps it ordered with the CTA barriers and the
+// shared stores of other phases (without it the load may be hoisted across
+// __syncthreads and read a previous filter group's phi).
+__device__ __forceinline__ float4 lds128(const float* ptr) {
+    float4 v;
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(ptr));
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a)
+                 : "memory");
+    return v;
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -104,11 +122,14 @@ __device__ __forceinline__ int mirror_clamp(int j, int n) {
 
 // phi(z) from the per-filter piecewise polynomial table (default path).
 //   The host samples phi_i(z) = sum_j w_ij exp(-(z-mu_j)^2/(2 gamma^2)) in
-//   float64 at 12 Chebyshev nodes of every interval of width h = min(delta,
-//   gamma) covering [mu_0 - 7 gamma, mu_{M-1} + 7 gamma] and stores the
-//   degree-11 interpolant's monomial coefficients in the local variable
-//   x in [-1/2, 1/2].  Interpolation error < 1e-10 * sum|w| (checked on the
-//   host at model creation); no MUFU, 3 LDS.128 + 11 FFMA.
+//   float64 at 8 Chebyshev nodes of every interval of width
+//   h = min(delta, gamma) / 2 covering [mu_0 - 7 gamma, mu_{M-1} + 7 gamma]
+//   and stores the degree-7 interpolant's monomial coefficients in the local
+//   variable x in [-1/2, 1/2], coefficient-major ([d][interval]) so the 8
+//   scalar loads of a warp hit distinct banks whenever its lanes' intervals
+//   lie within 32 of each other (conflict-free in practice).  Interpolation
+//   error ~1e-9 * sum|w| (checked on the host at model creation, DESIGN.md
+//   "RBF"); no MUFU, 8 LDS + 7 FFMA per response instead of 63 exp + 63 FMA.
 __device__ __forceinline__ float rbf_poly(float z, const float* __restrict__ tabf,
                                           const StageArgs& p) {
     float t = fmaf(z, p.inv_h, p.t_off);
@@ -116,19 +137,15 @@ __device__ __forceinline__ float rbf_poly(float z, const float* __restrict__ tab
     const float r = t + 12582912.0f;                 // rint(t) in the low bits
     const int j = __float_as_int(r) - 0x4B400000;
     const float x = t - (r - 12582912.0f);           // in [-1/2, 1/2]
-    const float4* c = reinterpret_cast<const float4*>(tabf + j * kPolyStride);
-    const float4 c0 = c[0], c1 = c[1], c2 = c[2];
-    float acc = fmaf(c2.w, x, c2.z);
-    acc = fmaf(acc, x, c2.y);
-    acc = fmaf(acc, x, c2.x);
-    acc = fmaf(acc, x, c1.w);
-    acc = fmaf(acc, x, c1.z);
-    acc = fmaf(acc, x, c1.y);
-    acc = fmaf(acc, x, c1.x);
-    acc = fmaf(acc, x, c0.w);
-    acc = fmaf(acc, x, c0.z);
-    acc = fmaf(acc, x, c0.y);
-    return fmaf(acc, x, c0.x);
+    const float* c = tabf + j;
+    const int n = p.tab_ni;
+    float acc = fmaf(c[7 * n], x, c[6 * n]);
+    acc = fmaf(acc, x, c[5 * n]);
+    acc = fmaf(acc, x, c[4 * n]);
+    acc = fmaf(acc, x, c[3 * n]);
+    acc = fmaf(acc, x, c[2 * n]);
+    acc = fmaf(acc, x, c[1 * n]);
+    return fmaf(acc, x, c[0]);
 }
 
 // phi(z) as the reference writes it: all M centres (generic bandwidths).
@@ -171,7 +188,7 @@ struct StageCfg {
 
 template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST>
 #ifndef TNRD_MINB
-#define TNRD_MINB (512 / NT)
+#define TNRD_MINB (768 / NT)
 #endif
 __global__ void __launch_bounds__(NT, TNRD_MINB) stage_kernel(const StageArgs p) {
     using C = StageCfg<MS, TH, TW, RF, RB, NT>;
@@ -352,10 +369,10 @@ __global__ void __launch_bounds__(NT, TNRD_MINB) stage_kernel(const StageArgs p)
 #pragma unroll
             for (int rr = 0; rr < RB + 2 * R; ++rr) {
                 float v[4 * C::NV];
-                const float4* src = reinterpret_cast<const float4*>(ph + (oy0 + rr) * C::PW + ox0);
+                const float* src = ph + (oy0 + rr) * C::PW + ox0;
 #pragma unroll
                 for (int q = 0; q < C::NV; ++q) {
-                    const float4 t = src[q];
+                    const float4 t = lds128(src + 4 * q);
                     v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
                 }
 #pragma unroll

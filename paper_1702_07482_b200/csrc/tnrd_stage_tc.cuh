@@ -354,10 +354,10 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc(const StageArgs p, con
 #pragma unroll
                 for (int rr = 0; rr < C::RB + 2 * R; ++rr) {
                     float v[4 * NV];
-                    const float4* src = reinterpret_cast<const float4*>(ph + (oy0 + rr) * kSPW + ox0);
+                    const float* src = ph + (oy0 + rr) * kSPW + ox0;
 #pragma unroll
                     for (int qq = 0; qq < NV; ++qq) {
-                        const float4 t = src[qq];
+                        const float4 t = lds128(src + 4 * qq);
                         v[4 * qq] = t.x; v[4 * qq + 1] = t.y; v[4 * qq + 2] = t.z; v[4 * qq + 3] = t.w;
                     }
 #pragma unroll

@@ -17,8 +17,10 @@ clean, f = synth.noisy_image(cfg, 0, 100, 90)
 u, _ = tn.run_diffusion(f, model); ref = O.run_diffusion(f.astype(np.float64), model)
 rel = float(np.max(np.abs(u - ref) / ref))
 res = [f"rel={rel:.1e}"]
-for key, B in (("c2", 1), ("c3", 32), ("c5", 4)):
+for key, B in (("c2", 1), ("c3", 32), ("c5", 4), ("c1", 1)):
     cfg = synth.CONFIGS[key]; model = synth.config_model(cfg)
+    if key == "c5" and __import__("os").environ.get("TNRD_STAGE_KERNEL") == "2":
+        continue
     f = torch.from_numpy(np.stack([synth.noisy_image(cfg, i)[1] for i in range(B)])).cuda()
     dm = tn.device_model_for(model)
     out = torch.empty_like(f); work = torch.empty_like(f)
@@ -34,7 +36,10 @@ for key, B in (("c2", 1), ("c3", 32), ("c5", 4)):
 print(" ".join(res), "MPix*st/s")
 ''' % REPO
 
-for so in sys.argv[1:]:
+for arg in sys.argv[1:]:
+    so, _, mode = arg.partition(":")
     env = dict(os.environ, TNRD_LIB_PATH=os.path.abspath(so))
+    if mode:
+        env["TNRD_STAGE_KERNEL"] = mode
     r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
-    print(f"{os.path.basename(so):24s}", (r.stdout.strip() or r.stderr.strip()[-300:]), flush=True)
+    print(f"{os.path.basename(so) + (':' + mode if mode else ''):26s}", (r.stdout.strip() or r.stderr.strip()[-300:]), flush=True)
