@@ -117,12 +117,12 @@ static double phi_exact(const double* w, int M, double mu0, double delta, double
 }
 
 // Degree-7 interpolant of phi on [zc - h/2, zc + h/2] at Chebyshev nodes,
-// as monomial coefficients in x = (z - zc)/h, written to out[d * ostride].
+// as monomial coefficients in x = (z - zc)/h, written to out[slot(d)].
 // Returns the max abs interpolation error (float64 coefficients) over 41
 // check points and, in *err32, the same with the fp32-rounded coefficients
 // the kernel uses.
 static double fit_interval(const double* w, int M, double mu0, double delta, double gamma,
-                           double zc, double h, float* out, int ostride, double* err32) {
+                           double zc, double h, float* out, int swap, double* err32) {
     constexpr int N = kPolyDeg + 1;
     long double A[N][N + 1];
     for (int k = 0; k < N; ++k) {
@@ -148,7 +148,7 @@ static double fit_interval(const double* w, int M, double mu0, double delta, dou
     for (int d = 0; d < N; ++d) {
         c[d] = (double)(A[d][N] / A[d][d]);
         c32[d] = (float)c[d];
-        out[(size_t)d * ostride] = c32[d];
+        out[swap ? (d ^ 4) : d] = c32[d];  // float4 halves swapped (bank spread)
     }
     double err = 0.0, e32 = 0.0;
     for (int k = 0; k <= 40; ++k) {
@@ -206,7 +206,7 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
     md->zlo = mu0 - 7.0 * gamma;
     const double zhi = mu0 + (M - 1) * delta + 7.0 * gamma;
     md->ni = (int)std::ceil((zhi - md->zlo) / md->h) + 1;
-    md->nip = round_up(md->ni, 4);
+    md->nip = md->ni;
     md->fast = (size_t)md->nip * kPolyN * kF <= 16384;  // <= 64 KB per group buffer
     md->tab_stride = md->fast ? md->nip * kPolyN : round_up(M, 4);
 
@@ -229,7 +229,7 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
                     md->fit_err = std::max(md->fit_err,
                                            fit_interval(w, M, mu0, delta, gamma,
                                                         md->zlo + q * md->h, md->h,
-                                                        tb + q, md->nip, &e32));
+                                                        tb + (size_t)q * kPolyN, (q >> 2) & 1, &e32));
                     md->fit_err32 = std::max(md->fit_err32, e32);
                 }
             } else {
@@ -238,11 +238,12 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
         }
     }
     // forward GEMM operand for the tensor-core kernel (kf = rot180(k), split
-    // into tf32 hi + lo), see tnrd_stage_tc.cuh
+    // into tf32 hi + lo, K-major), see tnrd_stage_tc.cuh
     std::vector<float> bop;
-    if (m <= 7) {
+    {
         const int ks = (m + 7) / 8, G = md->nk_pad / tc::kG;
-        md->bop_stage = (size_t)G * m * ks * 2 * 2 * tc::kG * 4;
+        const size_t bo = 2 * tc::kG * 4;                       // floats per (a, kk, prec)
+        md->bop_stage = (size_t)G * m * ks * 2 * bo;
         bop.assign(md->bop_stage * T, 0.0f);
         for (int t = 0; t < T; ++t)
             for (int g = 0; g < G; ++g)
@@ -251,16 +252,15 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
                         for (int kc = 0; kc < 2; ++kc)
                             for (int n = 0; n < tc::kG; ++n)
                                 for (int e = 0; e < 4; ++e) {
-                                    const int i = g * tc::kG + n, b = 8 * kk + 4 * kc + e;
+                                    const int f = g * tc::kG + n, b = 8 * kk + 4 * kc + e;
                                     float v = 0.0f;
-                                    if (i < nk && b < m)
-                                        v = (float)kernels[(((size_t)t * nk + i) * m + (m - 1 - a)) * m + (m - 1 - b)];
+                                    if (f < nk && b < m)
+                                        v = (float)kernels[(((size_t)t * nk + f) * m + (m - 1 - a)) * m + (m - 1 - b)];
                                     const float hi = tf32_rna_host(v);
                                     const size_t base = (size_t)t * md->bop_stage +
-                                        ((((size_t)g * m + a) * ks + kk) * 2) * (2 * tc::kG * 4);
+                                                        ((((size_t)g * m + a) * ks + kk) * 2) * bo;
                                     bop[base + (kc * tc::kG + n) * 4 + e] = hi;
-                                    bop[base + 2 * tc::kG * 4 + (kc * tc::kG + n) * 4 + e] =
-                                        tf32_rna_host(v - hi);
+                                    bop[base + bo + (kc * tc::kG + n) * 4 + e] = tf32_rna_host(v - hi);
                                 }
     }
     {
@@ -400,7 +400,8 @@ struct StageKernel {
 template <int MS>
 struct StageKernelTC {
     using C = tc::TcCfg<MS>;
-    static bool fits(int tab_stride) { return C::smem_bytes(tab_stride) <= 227 * 1024; }
+    // two CTAs per SM (TMEM: 2 x 256 columns)
+    static bool fits(int tab_stride) { return C::smem_bytes(tab_stride) <= 112 * 1024; }
     static int launch(const StageArgs& a, const float* bop, int batch, cudaStream_t s) {
         static std::mutex mu;
         static uint64_t attr_set = 0;
@@ -412,7 +413,7 @@ struct StageKernelTC {
             std::lock_guard<std::mutex> lk(mu);
             if (!(attr_set & (1ull << (dev & 63)))) {
                 CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              227 * 1024));
+                                              112 * 1024));
                 attr_set |= 1ull << (dev & 63);
             }
         }
@@ -430,6 +431,7 @@ static bool tc_supported(const tnrd_model* md) {
         case 3: return StageKernelTC<3>::fits(md->tab_stride);
         case 5: return StageKernelTC<5>::fits(md->tab_stride);
         case 7: return StageKernelTC<7>::fits(md->tab_stride);
+        case 9: return StageKernelTC<9>::fits(md->tab_stride);
         default: return false;
     }
 }
@@ -441,6 +443,7 @@ static int dispatch_tc(const tnrd_model* md, int t, StageArgs a, int batch, cuda
         case 3: return StageKernelTC<3>::launch(a, bop, batch, s);
         case 5: return StageKernelTC<5>::launch(a, bop, batch, s);
         case 7: return StageKernelTC<7>::launch(a, bop, batch, s);
+        case 9: return StageKernelTC<9>::launch(a, bop, batch, s);
         default: return fail(TNRD_EUNSUPPORTED, "no tensor-core stage kernel for m=%d", md->m);
     }
 }

@@ -69,7 +69,7 @@ struct StageArgs {
     float c8;            // 8 a lam
     float inv2a;         // 1 / (2a)
     // RBF: polynomial table (default) -- t = z / h + t_off, clamp [0, tmax];
-    // coefficient d of interval j at tab[d * tab_ni + j]
+    // interval j at tab[8 j], halves swapped when bit 2 of j is set
     float inv_h;
     int tab_ni;
     float t_off;
@@ -125,11 +125,12 @@ __device__ __forceinline__ int mirror_clamp(int j, int n) {
 //   float64 at 8 Chebyshev nodes of every interval of width
 //   h = min(delta, gamma) / 2 covering [mu_0 - 7 gamma, mu_{M-1} + 7 gamma]
 //   and stores the degree-7 interpolant's monomial coefficients in the local
-//   variable x in [-1/2, 1/2], coefficient-major ([d][interval]) so the 8
-//   scalar loads of a warp hit distinct banks whenever its lanes' intervals
-//   lie within 32 of each other (conflict-free in practice).  Interpolation
-//   error ~1e-9 * sum|w| (checked on the host at model creation, DESIGN.md
-//   "RBF"); no MUFU, 8 LDS + 7 FFMA per response instead of 63 exp + 63 FMA.
+//   variable x in [-1/2, 1/2]: interval j holds 8 floats, the two float4
+//   halves swapped when bit 2 of j is set, so that the 16-byte loads of 8
+//   lanes whose intervals are consecutive hit 8 distinct bank quads.
+//   Interpolation error ~1e-9 * sum|w| (checked on the host at model
+//   creation); no MUFU, 2 LDS.128 + 7 FFMA per response
+//   instead of 63 exp + 63 FMA.
 __device__ __forceinline__ float rbf_poly(float z, const float* __restrict__ tabf,
                                           const StageArgs& p) {
     float t = fmaf(z, p.inv_h, p.t_off);
@@ -137,15 +138,17 @@ __device__ __forceinline__ float rbf_poly(float z, const float* __restrict__ tab
     const float r = t + 12582912.0f;                 // rint(t) in the low bits
     const int j = __float_as_int(r) - 0x4B400000;
     const float x = t - (r - 12582912.0f);           // in [-1/2, 1/2]
-    const float* c = tabf + j;
-    const int n = p.tab_ni;
-    float acc = fmaf(c[7 * n], x, c[6 * n]);
-    acc = fmaf(acc, x, c[5 * n]);
-    acc = fmaf(acc, x, c[4 * n]);
-    acc = fmaf(acc, x, c[3 * n]);
-    acc = fmaf(acc, x, c[2 * n]);
-    acc = fmaf(acc, x, c[1 * n]);
-    return fmaf(acc, x, c[0]);
+    const int sw = (j >> 2) & 1;
+    const float* c = tabf + j * kPolyN;
+    const float4 lo = *reinterpret_cast<const float4*>(c + 4 * sw);        // c0..c3
+    const float4 hi = *reinterpret_cast<const float4*>(c + 4 * (sw ^ 1));  // c4..c7
+    float acc = fmaf(hi.w, x, hi.z);
+    acc = fmaf(acc, x, hi.y);
+    acc = fmaf(acc, x, hi.x);
+    acc = fmaf(acc, x, lo.w);
+    acc = fmaf(acc, x, lo.z);
+    acc = fmaf(acc, x, lo.y);
+    return fmaf(acc, x, lo.x);
 }
 
 // phi(z) as the reference writes it: all M centres (generic bandwidths).
@@ -331,11 +334,31 @@ __global__ void __launch_bounds__(NT, TNRD_MINB) stage_kernel(const StageArgs p)
 
         // ---- phi halo outside the image = mirror of in-image phi -------------
         if (need_fix) {
-            // phi-region (py, px) <-> image (Y0 - R + py, X0 - R + px)
-            for (int i = tid; i < kF * C::SPHI; i += NT) {
-                const int fi = i / C::SPHI;
-                const int rem = i - fi * C::SPHI;
-                const int py = rem / C::PW, px = rem - py * C::PW;
+            // only the out-of-image band of the phi region is rewritten: rows
+            // [0, nt) and [h0, C::PH) and, for the rows in between, columns
+            // [0, nl) and [w0, C::PW); sources are in-image (mirror).
+            const int nt_ = fix_t ? min(R, C::PH) : 0;
+            const int h0 = fix_b ? max(nt_, min(C::PH, p.H - (Y0 - R))) : C::PH;
+            const int nl_ = fix_l ? R : 0;
+            const int w0 = fix_r ? max(nl_, min(C::PW, p.W - (X0 - R))) : C::PW;
+            const int full_rows = nt_ + (C::PH - h0);
+            const int mid_rows = h0 - nt_;
+            const int per_f = full_rows * C::PW + mid_rows * (nl_ + C::PW - w0);
+            for (int i = tid; i < kF * per_f; i += NT) {
+                const int j = i / per_f;
+                int rem = i - j * per_f;
+                int py, px;
+                if (rem < full_rows * C::PW) {
+                    const int rr = rem / C::PW;
+                    px = rem - rr * C::PW;
+                    py = rr < nt_ ? rr : h0 + (rr - nt_);
+                } else {
+                    rem -= full_rows * C::PW;
+                    const int wcols = nl_ + C::PW - w0;
+                    const int rr = rem / wcols, cc = rem - rr * wcols;
+                    py = nt_ + rr;
+                    px = cc < nl_ ? cc : w0 + (cc - nl_);
+                }
                 const int Y = Y0 - R + py, X = X0 - R + px;
                 int sy = Y, sx = X;
                 if (X < 0 && X >= -R) sx = -1 - X;
@@ -344,7 +367,7 @@ __global__ void __launch_bounds__(NT, TNRD_MINB) stage_kernel(const StageArgs p)
                 else if (!bot_halo && Y >= p.H && Y < p.H + R) sy = 2 * p.H - 1 - Y;
                 if (sy != Y || sx != X) {
                     const int spy = sy - (Y0 - R), spx = sx - (X0 - R);
-                    sPhi[fi * C::SPHI + py * C::PW + px] = sPhi[fi * C::SPHI + spy * C::PW + spx];
+                    sPhi[j * C::SPHI + py * C::PW + px] = sPhi[j * C::SPHI + spy * C::PW + spx];
                 }
             }
             __syncthreads();

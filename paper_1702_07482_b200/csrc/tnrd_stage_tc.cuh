@@ -6,20 +6,25 @@
 // moves from FFMA to tcgen05:
 //
 //   * the 49-tap stencil is a GEMM D[points x 16 filters] = A[points x taps]
-//     B[taps x 16 filters] per filter group.  No im2col: for tap row a and
-//     point class o = x mod 4, the A rows of 8 consecutive class-o points of
-//     one image row are the overlapping 16-byte windows u[y+a][4k+o .. 4k+o+7]
+//     B[taps x 16 filters] per batch of 16 filters.  No im2col: for tap row a
+//     and point class o = x mod 4, the A rows of the 8 class-o points of one
+//     image row are the overlapping 32-byte windows u[y+a][4k+o .. 4k+o+7]
 //     of a class-shifted copy of the u row, i.e. exactly a K-major
-//     SWIZZLE_NONE core matrix with rows 16 B apart, LBO = 16 B (the second
-//     K-chunk starts one window later) and SBO = the copy's row stride.  One
+//     SWIZZLE_NONE core matrix with rows 16 B apart (LBO = 16 B: the second
+//     K-chunk starts one window later; SBO = the copy's row stride).  One
 //     M=128 MMA covers 16 image rows x 8 class-o points of the 32-column phi
 //     region; a 32 x 32 region = 2 bands x 4 classes = 8 MMA blocks.
+//     (MN-major tf32 B operands, which would let one copy serve all classes,
+//     produced all-zero accumulators on this B200/driver in
+//     tools/probes/mma_mn_probe.cu, so the classes are separate copies.)
 //   * 3xTF32: u = u_hi + u_lo, k = k_hi + k_lo (hi = cvt.rna.tf32), D +=
 //     hi*hi + lo*hi + hi*lo with fp32 accumulation in TMEM (~2^-21 relative,
 //     single-pass TF32 fails the 1e-4 bar, 3xTF32 passes).
-//   * accumulators live in TMEM (2 x 128 columns, double-buffered by filter
-//     group so the tensor core computes group g+1 while the CUDA cores run
-//     the RBF + backward pass of group g); commit -> mbarrier -> tcgen05.ld.
+//   * accumulators live in TMEM (2 x 128 columns, double-buffered by batch
+//     so the tensor core computes batch b+1 while the CUDA cores run the RBF
+//     + backward pass of batch b, 4 filters at a time); commit -> mbarrier ->
+//     tcgen05.ld.  109 KB of shared memory and 256 TMEM columns per CTA: two
+//     CTAs per SM.
 //   * RBF, phi mirror fix-up, backward correlation and the prox epilogue are
 //     the CUDA-core code of tnrd_stage.cuh.
 #pragma once
@@ -28,13 +33,14 @@
 namespace tnrd {
 namespace tc {
 
-constexpr int kG = 16;           // filters per group (MMA N)
+constexpr int kG = 16;           // filters per MMA batch (MMA N)
+constexpr int kS = 4;            // filters per RBF/backward sub-group
 constexpr int kPW = 32;          // phi-region width (4 classes x 8 points)
 constexpr int kPH = 32;          // phi-region height (2 bands of 16 rows)
 constexpr int kBlocks = 8;       // 2 bands x 4 classes, M = 128 each
 constexpr int kSPW = 36;         // sPhi row stride (floats)
-constexpr int kNT = 384;         // 12 warps = 3 warpgroups
-constexpr int kNSPLIT = 4;       // backward filter split (4 filters each)
+constexpr int kNT = 256;         // 8 warps = 2 warpgroups
+constexpr int kNSPLIT = 2;       // backward filter split (2 filters each)
 constexpr int kTmemCols = 256;   // 2 buffers x 8 blocks x 16 columns
 
 // instruction descriptor: kind::tf32, D f32, A/B tf32 K-major, M=128, N=16
@@ -89,58 +95,54 @@ __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::be
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* v) {
+    uint32_t r[4];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+    for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// Host-prepared per-stage operand for the forward GEMM (built by
-// tnrd_model_create): for group g, ksteps kk (b = 8kk .. 8kk+7), tap row a,
-// precision p (0 hi, 1 lo): [kc (2)][n (16)][4 floats] = kf_n[a][8kk+4kc+..]
-// with kf = rot180(k) the correlation form of the true convolution.
+// Host-prepared forward GEMM operand per stage (tnrd_model_create): for
+// batch b, tap row a, K-step kk (b = 8kk .. 8kk+7), precision p (0 hi, 1 lo):
+// K-major [kc (2)][n (16)][4] = kf_n[a][8kk + 4kc + e] (zero for b >= m),
+// kf = rot180(k) the correlation form of the true convolution.
 template <int MS>
 struct TcCfg {
     static constexpr int R = MS / 2;
     static constexpr int KSTEPS = (MS + 7) / 8;           // K = 8 per MMA
-    static constexpr int TH = (MS == 9) ? 24 : 26;        // output tile
+    static constexpr int TH = (MS == 9) ? 24 : (MS == 7 ? 26 : (MS == 5 ? 28 : 30));
     static constexpr int TW = (MS == 9) ? 24 : (MS == 7 ? 26 : 28);
     static constexpr int RB = 2;
     static constexpr int OBX = (TW + 3) / 4;
-    static constexpr int OBY = TH / RB;
+    static constexpr int OBY = (TH + RB - 1) / RB;
     static constexpr int ITEMS = OBX * OBY * kNSPLIT;
     static_assert(ITEMS <= kNT, "backward items must fit the CTA");
     static_assert(TH + 2 * R <= kPH && TW + 2 * R <= kPW, "tile + halo must fit the phi region");
-    static_assert(4 * OBX + 2 * R <= kSPW, "backward reads past the phi row stride");
+    static_assert(4 * OBX + 2 * R <= kSPW && RB * OBY + 2 * R <= kPH, "backward reads outside sPhi");
     static constexpr int UR = kPH + 2 * R;                // u rows
     static constexpr int CW = 32 + 8 * KSTEPS - 4;        // class-copy width (floats)
     static constexpr int CS = round_up(CW, 4);            // class-copy row stride
     static constexpr int COPY = UR * CS;                  // floats per class copy
-    static constexpr int BOP = 2 * kG * 4;                // floats per (a, kk, p) B operand
-    static constexpr int BGROUP = MS * KSTEPS * 2 * BOP;  // floats per group
+    static constexpr int BOP = 2 * kG * 4;                // floats per (a, kk, prec) operand
+    static constexpr int BBATCH = MS * KSTEPS * 2 * BOP;  // floats per batch
     static constexpr int KP = round_up(MS * MS, 4);
     static constexpr int SPHI = kPH * kSPW;
     // shared layout (floats)
-    static constexpr int OFF_COPY = 0;                              // [4 classes][2 prec][COPY]
-    static constexpr int OFF_B = OFF_COPY + 8 * COPY;               // [2 buf][BGROUP]
-    static constexpr int OFF_TAP = OFF_B + 2 * BGROUP;              // [2 buf][kG][KP]
-    static constexpr int OFF_PHI = OFF_TAP + 2 * kG * KP;           // [kG][SPHI]
-    static constexpr int OFF_TAB = OFF_PHI + kG * SPHI;             // [kG][tab_stride]
+    static constexpr int OFF_COPY = 0;                    // [4 classes][2 prec][COPY]
+    static constexpr int OFF_B = OFF_COPY + 8 * COPY;     // [2 buf][BBATCH]
+    static constexpr int OFF_TAP = OFF_B + 2 * BBATCH;    // [2 buf][kS][KP]
+    static constexpr int OFF_PHI = OFF_TAP + 2 * kS * KP; // [kS][SPHI]
+    static constexpr int OFF_TAB = OFF_PHI + kS * SPHI;   // [kS][tab_stride]
     static size_t smem_bytes(int tab_stride) {
-        return sizeof(float) * (size_t)(OFF_TAB + kG * tab_stride) + 64;  // + barriers
+        return sizeof(float) * (size_t)(OFF_TAB + kS * tab_stride) + 64;  // + barriers
     }
 };
 
 template <int MS>
-__global__ void __launch_bounds__(kNT, 1) stage_kernel_tc(const StageArgs p, const float* __restrict__ bop) {
+__global__ void __launch_bounds__(kNT, 2) stage_kernel_tc(const StageArgs p, const float* __restrict__ bop) {
     using C = TcCfg<MS>;
     constexpr int R = C::R;
     extern __shared__ __align__(128) float smem[];
@@ -149,7 +151,8 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc(const StageArgs p, con
     float* sTap = smem + C::OFF_TAP;
     float* sPhi = smem + C::OFF_PHI;
     float* sTab = smem + C::OFF_TAB;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sTab + kG * p.tab_stride);  // [2] mma done
+    const int tabsz = kS * p.tab_stride;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sTab + tabsz);  // [2] batch MMAs done
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
 
     const int tid = threadIdx.x;
@@ -162,24 +165,23 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc(const StageArgs p, con
     float* __restrict__ uout = p.u_out + (int64_t)img * p.img_stride;
     const bool top_halo = p.flags & 0x2u;
     const bool bot_halo = p.flags & 0x4u;
-    const int ngroups = p.ngroups;  // of kG filters
+    const int nbatch = p.ngroups;                 // batches of kG filters
+    const int nsub = (p.nk + kS - 1) / kS;        // real sub-groups of kS filters
 
-    auto prefetch_b = [&](int g, int buf) {  // forward GEMM operand of group g
-        const float* gb = bop + (size_t)g * C::BGROUP;
-        float* sb = sB + buf * C::BGROUP;
-        for (int i = tid; i < C::BGROUP / 4; i += kNT) cp_async16(sb + 4 * i, gb + 4 * i);
+    auto prefetch_b = [&](int b, int buf) {       // forward GEMM operand of batch b
+        const float* gb = bop + (size_t)b * C::BBATCH;
+        float* sb = sB + buf * C::BBATCH;
+        for (int i = tid; i < C::BBATCH / 4; i += kNT) cp_async16(sb + 4 * i, gb + 4 * i);
     };
-    auto prefetch_taps = [&](int g, int buf) {  // backward taps of group g
-        const float* gt = p.taps + (size_t)g * kG * C::KP;
-        float* st = sTap + buf * kG * C::KP;
-        for (int i = tid; i < kG * C::KP / 4; i += kNT) cp_async16(st + 4 * i, gt + 4 * i);
-    };
-    auto prefetch_tab = [&](int g) {
-        const float* gb = p.tab + (size_t)g * kG * p.tab_stride;
-        for (int i = tid; i < kG * p.tab_stride / 4; i += kNT) cp_async16(sTab + 4 * i, gb + 4 * i);
+    auto prefetch_sub = [&](int sg, int buf) {    // taps + RBF tables of sub-group sg
+        const float* gt = p.taps + (size_t)sg * kS * C::KP;
+        float* st = sTap + buf * kS * C::KP;
+        for (int i = tid; i < kS * C::KP / 4; i += kNT) cp_async16(st + 4 * i, gt + 4 * i);
+        const float* gb = p.tab + (size_t)sg * tabsz;   // single buffer: used only by the RBF phase
+        for (int i = tid; i < tabsz / 4; i += kNT) cp_async16(sTab + 4 * i, gb + 4 * i);
     };
 
-    // ---- setup: barriers, TMEM, operands of group 0 -------------------------
+    // ---- setup: barriers, TMEM, operands ------------------------------------
     if (tid == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -192,14 +194,15 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc(const StageArgs p, con
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     prefetch_b(0, 0);
-    if (ngroups > 1) prefetch_b(1, 1);
-    prefetch_taps(0, 0);
-    prefetch_tab(0);
+    if (nbatch > 1) prefetch_b(1, 1);
+    prefetch_sub(0, 0);
     cp_async_commit();
 
-    // u region (2r halo), staged in sPhi (free until the first RBF phase)
-    constexpr int UW = C::CW + 3;  // u_reg columns needed by the class copies
+    // A operand: u region (2r halo), staged in sPhi (free until the first
+    // RBF phase), then class copies copy[o][prec][ur][j] = hi/lo(u_reg[ur][j + o])
+    constexpr int UW = C::CW + 3;
     float* sU = sPhi;
+    static_assert(C::UR * UW <= kS * C::SPHI, "u staging must fit sPhi");
     {
         const bool floor_in = p.flags & 0x1u;
         for (int i = tid; i < C::UR * UW; i += kNT) {
@@ -214,10 +217,9 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc(const StageArgs p, con
         }
     }
     __syncthreads();
-    // class copies: copy[o][prec][ur][j] = hi/lo(u_reg[ur][j + o])
-    for (int i = tid; i < 4 * C::UR * C::CS; i += kNT) {
-        const int o = i / (C::UR * C::CS);
-        const int rem = i - o * (C::UR * C::CS);
+    for (int i = tid; i < 4 * C::COPY; i += kNT) {
+        const int o = i / C::COPY;
+        const int rem = i - o * C::COPY;
         const int ur = rem / C::CS, j = rem - ur * C::CS;
         const float u = (j < C::CW) ? sU[ur * UW + j + o] : 0.0f;
         const float hi = tf32_rna(u);
@@ -231,34 +233,37 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc(const StageArgs p, con
     fence_after();
     const uint32_t tmem = *tmem_slot;
 
-
-    // one elected thread issues the 8 blocks x taps x 3 passes of group g
-    auto issue_group = [&](int g) {
-        const int buf = g & 1;
-        const float* sb = sB + buf * C::BGROUP;
-        for (int blk = 0; blk < kBlocks; ++blk) {
-            const int band = blk >> 2, o = blk & 3;
-            const uint32_t d = tmem + (uint32_t)(buf * 128 + blk * kG);
-            int first = 1;
+    // one elected thread issues batch b: 2 bands x m taps x K-steps x 3
+    // passes x 4 classes (classes innermost: consecutive MMAs hit different
+    // accumulators)
+    auto issue_batch = [&](int b) {
+        const int buf = b & 1;
+        const float* sb = sB + buf * C::BBATCH;
+        for (int band = 0; band < 2; ++band) {
             for (int a = 0; a < MS; ++a) {
                 for (int kk = 0; kk < C::KSTEPS; ++kk) {
                     const uint32_t arow = (uint32_t)((16 * band + a) * C::CS + 8 * kk) * 4u;
-                    const uint64_t ahi = make_desc(smem_u32(sCopy + (o * 2 + 0) * C::COPY) + arow, 16, C::CS * 4);
-                    const uint64_t alo = make_desc(smem_u32(sCopy + (o * 2 + 1) * C::COPY) + arow, 16, C::CS * 4);
                     const float* bb = sb + ((a * C::KSTEPS + kk) * 2) * C::BOP;
                     const uint64_t bhi = make_desc(smem_u32(bb), kG * 16, 128);
                     const uint64_t blo = make_desc(smem_u32(bb + C::BOP), kG * 16, 128);
-                    mma_tf32(d, ahi, bhi, first ? 0u : 1u);
-                    mma_tf32(d, alo, bhi, 1u);
-                    mma_tf32(d, ahi, blo, 1u);
-                    first = 0;
+#pragma unroll
+                    for (int pass = 0; pass < 3; ++pass) {
+#pragma unroll
+                        for (int o = 0; o < 4; ++o) {
+                            const int prec = pass == 1 ? 1 : 0;
+                            const uint64_t ad = make_desc(smem_u32(sCopy + (o * 2 + prec) * C::COPY) + arow,
+                                                          16, C::CS * 4);
+                            const uint32_t d = tmem + (uint32_t)(buf * 128 + (band * 4 + o) * kG);
+                            const uint32_t acc = (a | kk | pass) ? 1u : 0u;
+                            mma_tf32(d, ad, pass == 2 ? blo : bhi, acc);
+                        }
+                    }
                 }
             }
         }
         mma_commit(&bars[buf]);
     };
-
-    if (tid == 0) issue_group(0);
+    if (tid == 0) issue_batch(0);
 
     // tile touches a mirrored image edge? (phi halo fix-up needed)
     const bool fix_l = X0 - R < 0;
@@ -278,45 +283,59 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc(const StageArgs p, con
         for (int c = 0; c < 4; ++c) force[r][c] = 0.0f;
 
     const int wg = warp >> 2, q = warp & 3;
-    for (int g = 0; g < ngroups; ++g) {
-        const int buf = g & 1;
-        // ---- z of group g ready in TMEM --------------------------------------
-        mbar_wait(&bars[buf], (g >> 1) & 1);
-        fence_after();
-        // ---- RBF: TMEM -> phi -> sPhi ----------------------------------------
-        for (int blk = wg; blk < kBlocks; blk += 3) {
-            float z[kG];
-            tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * 128 + blk * kG), z);
+    for (int sg = 0; sg < nsub; ++sg) {
+        const int b = sg / (kG / kS), s = sg % (kG / kS), sbuf = sg & 1;
+        if (s == 0) {
+            mbar_wait(&bars[b & 1], (b >> 1) & 1);   // batch b in TMEM
+            fence_after();
+            if (b + 2 < nbatch) prefetch_b(b + 2, b & 1);  // its B buffer is free now
+            cp_async_commit();
+            if (tid == 0 && b + 1 < nbatch) issue_batch(b + 1);
+        }
+        // ---- RBF: TMEM -> phi -> sPhi (4 filters) ----------------------------
+        const float* tabg = sTab;
+#pragma unroll 1
+        for (int blk = wg; blk < kBlocks; blk += 2) {
+            float z[kS];
+            tmem_ld4(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)((b & 1) * 128 + blk * kG + s * kS), z);
             const int row = 32 * q + lane;
             const int py = 16 * (blk >> 2) + (row >> 3);
             const int px = 4 * (row & 7) + (blk & 3);
 #pragma unroll
-            for (int j = 0; j < kG; ++j) {
-                if (g * kG + j < p.nk)
-                    sPhi[j * C::SPHI + py * kSPW + px] = rbf_poly(z[j], sTab + j * p.tab_stride, p);
-            }
+            for (int j = 0; j < kS; ++j)
+                sPhi[j * C::SPHI + py * kSPW + px] = rbf_poly(z[j], tabg + j * p.tab_stride, p);
         }
         fence_before();
-        __syncthreads();  // sPhi complete; TMEM buffer `buf` drained; B[buf] free
-        // tables + taps of group g+1 and the GEMM operand of group g+2 stream
-        // in during the backward pass
-        if (g + 2 < ngroups) prefetch_b(g + 2, buf);
-        if (g + 1 < ngroups) {
-            prefetch_taps(g + 1, buf ^ 1);
-            prefetch_tab(g + 1);
-        }
+        __syncthreads();  // sPhi complete; tables of sg and taps of sg-1 free
+        if (sg + 1 < nsub) prefetch_sub(sg + 1, sbuf ^ 1);   // lands during the bwd
         cp_async_commit();
-        if (tid == 0 && g + 1 < ngroups) {
-            fence_after();
-            issue_group(g + 1);  // B[(g+1)&1] landed at the previous barrier
-        }
         // ---- phi halo outside the image = mirror of in-image phi -------------
         if (need_fix) {
-            for (int i = tid; i < kG * C::SPHI; i += kNT) {
-                const int j = i / C::SPHI;
-                const int rem = i - j * C::SPHI;
-                const int py = rem / kSPW, px = rem - py * kSPW;
-                if (px >= kPW) continue;
+            // only the out-of-image band of the phi region is rewritten: rows
+            // [0, nt) and [h0, kPH) and, for the rows in between, columns
+            // [0, nl) and [w0, kPW); sources are in-image (mirror).
+            const int nt_ = fix_t ? min(R, kPH) : 0;
+            const int h0 = fix_b ? max(nt_, min(kPH, p.H - (Y0 - R))) : kPH;
+            const int nl_ = fix_l ? R : 0;
+            const int w0 = fix_r ? max(nl_, min(kPW, p.W - (X0 - R))) : kPW;
+            const int full_rows = nt_ + (kPH - h0);
+            const int mid_rows = h0 - nt_;
+            const int per_f = full_rows * kPW + mid_rows * (nl_ + kPW - w0);
+            for (int i = tid; i < kS * per_f; i += kNT) {
+                const int j = i / per_f;
+                int rem = i - j * per_f;
+                int py, px;
+                if (rem < full_rows * kPW) {
+                    const int rr = rem / kPW;
+                    px = rem - rr * kPW;
+                    py = rr < nt_ ? rr : h0 + (rr - nt_);
+                } else {
+                    rem -= full_rows * kPW;
+                    const int wcols = nl_ + kPW - w0;
+                    const int rr = rem / wcols, cc = rem - rr * wcols;
+                    py = nt_ + rr;
+                    px = cc < nl_ ? cc : w0 + (cc - nl_);
+                }
                 const int Y = Y0 - R + py, X = X0 - R + px;
                 int sy = Y, sx = X;
                 if (X < 0 && X >= -R) sx = -1 - X;
@@ -330,13 +349,13 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc(const StageArgs p, con
             }
             __syncthreads();
         }
-        // ---- backward: force += corr(phi_j, k_j), 4 filters per item ---------
+        // ---- backward: force += corr(phi_j, k_j), 2 filters per item ---------
         if (has_item) {
-            const float* tapg = sTap + buf * kG * C::KP;
+            const float* tapg = sTap + sbuf * kS * C::KP;
 #pragma unroll 1
-            for (int jj = 0; jj < kG / kNSPLIT; ++jj) {
-                const int j = split * (kG / kNSPLIT) + jj;
-                if (g * kG + j >= p.nk) break;
+            for (int jj = 0; jj < kS / kNSPLIT; ++jj) {
+                const int j = split * (kS / kNSPLIT) + jj;
+                if (sg * kS + j >= p.nk) break;
                 float k[MS * MS];
                 {
                     const float4* t4 = reinterpret_cast<const float4*>(tapg + j * C::KP);
@@ -365,10 +384,10 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc(const StageArgs p, con
                         const int ro = rr - a;
                         if (ro >= 0 && ro < C::RB) {
 #pragma unroll
-                            for (int b = 0; b < MS; ++b) {
-                                const float kk = k[a * MS + b];
+                            for (int bb = 0; bb < MS; ++bb) {
+                                const float kk = k[a * MS + bb];
 #pragma unroll
-                                for (int c = 0; c < 4; ++c) force[ro][c] = fmaf(kk, v[c + b], force[ro][c]);
+                                for (int c = 0; c < 4; ++c) force[ro][c] = fmaf(kk, v[c + bb], force[ro][c]);
                             }
                         }
                     }
@@ -377,10 +396,10 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc(const StageArgs p, con
         }
         cp_async_wait_all();
         fence_async_smem();
-        __syncthreads();  // bwd done with sPhi/taps; next tables + B landed
+        __syncthreads();  // bwd done with sPhi/taps; next tables/taps/B landed
     }
 
-    // ---- release TMEM --------------------------------------------------------
+    // ---- release TMEM (all batches were waited on) ------------------------------
     fence_before();
     __syncthreads();
     if (warp == 0) {
@@ -414,7 +433,7 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc(const StageArgs p, con
 #pragma unroll
     for (int r = 0; r < C::RB; ++r) {
         const int oy = oy0 + r, Y = Y0 + oy;
-        if (Y >= p.H) continue;
+        if (oy >= C::TH || Y >= p.H) continue;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const int ox = ox0 + c, X = X0 + ox;
@@ -423,7 +442,7 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc(const StageArgs p, con
             if (out_force) {
                 res = force[r][c];
             } else {
-                float u = __ldg(uin + (int64_t)Y * p.ld + X);  // exact u (copies are split)
+                float u = __ldg(uin + (int64_t)Y * p.ld + X);  // exact u (the copies are split)
                 if (p.flags & 0x1u) u = fmaxf(u, kFFloor);
                 const float fv = __ldg(fin + (int64_t)Y * p.ld + X);
                 if (check_f) {
