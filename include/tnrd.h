@@ -92,7 +92,8 @@ int tnrd_model_rbf_fit(const tnrd_model* model, double* max_abs_err,
 /* Stage kernel selection (process-wide): 0 = auto (the kernel measured
  * fastest on B200), 1 = CUDA-core kernel, 2 = tcgen05
  * forward-GEMM kernel (error if the model is unsupported: m > 7 or RBF
- * tables too large). */
+ * tables too large), 3 / 4 = CUDA-core kernel with its small (32x32) /
+ * large (64x64) tile configuration forced. */
 int tnrd_set_stage_kernel(int mode);
 
 /* Reset a device status block (stream-ordered memset). */

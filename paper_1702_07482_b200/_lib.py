@@ -128,10 +128,12 @@ def dptr(a) -> _dp:
 
 
 KERNEL_AUTO, KERNEL_CUDA_CORE, KERNEL_TENSOR_CORE = 0, 1, 2
+KERNEL_SMALL_TILES, KERNEL_LARGE_TILES = 3, 4
 
 
 def set_stage_kernel(mode: int) -> None:
-    """0 auto (tcgen05 forward GEMM where supported), 1 CUDA-core, 2 tcgen05."""
+    """0 auto, 1 CUDA-core, 2 tcgen05 forward GEMM, 3/4 CUDA-core with
+    small/large tiles forced."""
     check(load().tnrd_set_stage_kernel(int(mode)))
 
 

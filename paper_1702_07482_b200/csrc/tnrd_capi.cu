@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <string>
 #include <vector>
 
@@ -87,11 +88,12 @@ struct tnrd_model {
 };
 
 // 0 = auto (the faster kernel as measured on B200: currently
-// the CUDA-core kernel), 1 = CUDA-core only, 2 = tensor-core required
+// the CUDA-core kernel), 1 = CUDA-core only, 2 = tensor-core required,
+// 3 / 4 = CUDA-core with small / large tiles forced (tests)
 static std::atomic<int> g_kernel_mode{0};
 
 extern "C" int tnrd_set_stage_kernel(int mode) {
-    if (mode < 0 || mode > 2) return fail(TNRD_EINVAL, "stage kernel mode must be 0, 1 or 2");
+    if (mode < 0 || mode > 4) return fail(TNRD_EINVAL, "stage kernel mode must be in 0..4");
     g_kernel_mode.store(mode);
     return TNRD_OK;
 }
@@ -352,27 +354,20 @@ extern "C" int tnrd_status_decode(const uint32_t* h, int* bad_stage) {
 
 // ----------------------------------------------------------------- stage launch
 
-#ifndef TNRD_TH
-#define TNRD_TH 32
-#endif
-#ifndef TNRD_TW
-#define TNRD_TW 32
-#endif
-#ifndef TNRD_RF
-#define TNRD_RF 2
-#endif
-#ifndef TNRD_RB
-#define TNRD_RB 2
-#endif
-#ifndef TNRD_NT
-#define TNRD_NT 256
-#endif
+// CUDA-core stage kernel configurations (tile, rows per forward block,
+// rows per backward block, threads, filters per group, min CTAs/SM), chosen
+// from the sweeps in DESIGN.md §5: small tiles keep a single 512^2 image
+// spread over all 148 SMs; large tiles cut the phi-halo recompute
+// (inflation 1.48 -> 1.23) once the grid has enough tiles.
+struct SmallTile { static constexpr int TH = 32, TW = 32, RF = 2, RB = 2, NT = 256, F = 4; };
+struct LargeTile { static constexpr int TH = 64, TW = 64, RF = 2, RB = 4, NT = 256, F = 2; };
 
-template <int MS, bool FAST>
+template <int MS, bool FAST, class T>
 struct StageKernel {
-    // tile choice; overridable at build time for sweeps
-    static constexpr int TH = TNRD_TH, TW = TNRD_TW, RF = TNRD_RF, RB = TNRD_RB, NT = TNRD_NT;
-    using C = StageCfg<MS, TH, TW, RF, RB, NT>;
+    static constexpr int TH = T::TH, TW = T::TW, RF = T::RF, RB = T::RB, NT = T::NT, F = T::F;
+    // 3 CTAs/SM fit the register file for m <= 7; m = 9 keeps 81 taps live
+    static constexpr int MINB = std::is_same<T, LargeTile>::value ? 2 : (MS >= 9 ? 2 : 3);
+    using C = StageCfg<MS, TH, TW, RF, RB, NT, F>;
 
     static int launch(const StageArgs& a, int batch, cudaStream_t s) {
         static std::mutex mu;
@@ -380,7 +375,7 @@ struct StageKernel {
         const size_t smem = C::smem_bytes(a.tab_stride);
         int dev = 0;
         cudaGetDevice(&dev);
-        auto kern = stage_kernel<MS, TH, TW, RF, RB, NT, FAST>;
+        auto kern = stage_kernel<MS, TH, TW, RF, RB, NT, FAST, F, MINB>;
         {
             std::lock_guard<std::mutex> lk(mu);
             if (!(attr_set & (1ull << (dev & 63)))) {
@@ -390,12 +385,40 @@ struct StageKernel {
             }
         }
         dim3 grid((a.W + TW - 1) / TW, (a.H + TH - 1) / TH, batch);
-        kern<<<grid, NT, smem, s>>>(a);
+        StageArgs b = a;
+        b.ngroups = (a.nk + F - 1) / F;
+        kern<<<grid, NT, smem, s>>>(b);
         CUDA_TRY(cudaGetLastError());
         g_launches.fetch_add(1);
         return TNRD_OK;
     }
 };
+
+// large tiles once they give >= 4 waves of 2 CTAs on 148 SMs
+static bool use_large_tiles(const StageArgs& a, int batch) {
+    const long tiles = (long)((a.W + LargeTile::TW - 1) / LargeTile::TW) *
+                       ((a.H + LargeTile::TH - 1) / LargeTile::TH) * batch;
+    return tiles >= 4L * 2 * 148;
+}
+
+template <bool FAST, class T>
+static int dispatch_m_t(int m, const StageArgs& a, int batch, cudaStream_t s) {
+    switch (m) {
+        case 3: return StageKernel<3, FAST, T>::launch(a, batch, s);
+        case 5: return StageKernel<5, FAST, T>::launch(a, batch, s);
+        case 7: return StageKernel<7, FAST, T>::launch(a, batch, s);
+        case 9: return StageKernel<9, FAST, T>::launch(a, batch, s);
+        default: return fail(TNRD_EUNSUPPORTED, "unsupported filter size %d", m);
+    }
+}
+
+template <bool FAST>
+static int dispatch_m(int m, const StageArgs& a, int batch, cudaStream_t s) {
+    const int mode = g_kernel_mode.load();
+    const bool large = mode == 4 || (mode != 3 && use_large_tiles(a, batch));
+    return large ? dispatch_m_t<FAST, LargeTile>(m, a, batch, s)
+                 : dispatch_m_t<FAST, SmallTile>(m, a, batch, s);
+}
 
 template <int MS>
 struct StageKernelTC {
@@ -448,16 +471,6 @@ static int dispatch_tc(const tnrd_model* md, int t, StageArgs a, int batch, cuda
     }
 }
 
-template <bool FAST>
-static int dispatch_m(int m, const StageArgs& a, int batch, cudaStream_t s) {
-    switch (m) {
-        case 3: return StageKernel<3, FAST>::launch(a, batch, s);
-        case 5: return StageKernel<5, FAST>::launch(a, batch, s);
-        case 7: return StageKernel<7, FAST>::launch(a, batch, s);
-        case 9: return StageKernel<9, FAST>::launch(a, batch, s);
-        default: return fail(TNRD_EUNSUPPORTED, "unsupported filter size %d", m);
-    }
-}
 
 static int check_shape(const tnrd_model* md, int batch, int H, int W, int64_t ld,
                        int64_t image_stride) {

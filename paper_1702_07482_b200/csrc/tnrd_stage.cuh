@@ -162,7 +162,7 @@ __device__ __forceinline__ float rbf_direct(float z, const float* __restrict__ w
     return s;
 }
 
-template <int MS, int TH, int TW, int RF, int RB, int NT>
+template <int MS, int TH, int TW, int RF, int RB, int NT, int F = kF>
 struct StageCfg {
     static constexpr int R = MS / 2;
     static constexpr int PH = round_up(TH + 2 * R, RF);  // phi rows computed
@@ -174,34 +174,33 @@ struct StageCfg {
     static constexpr int KP = round_up(KK, 4);
     static constexpr int NBX = PW / 4;                   // forward blocks per row
     static constexpr int NBY = PH / RF;
-    static constexpr int FWD_ITEMS = NBX * NBY * kF;
+    static constexpr int NBLK = NBX * NBY;               // forward blocks per filter
+    static constexpr int TPF = NT / F;                   // forward threads per filter
+    static_assert(TPF * F == NT, "forward threads must split evenly over the filters");
     static constexpr int OBX = TW / 4;                   // output blocks
     static constexpr int OBY = TH / RB;
     static constexpr int NSPLIT = NT / (OBX * OBY);      // bwd filter split
-    static_assert(OBX * OBY * NSPLIT == NT && kF % NSPLIT == 0,
+    static_assert(OBX * OBY * NSPLIT == NT && F % NSPLIT == 0,
                   "output blocks x filter split must cover the CTA");
     static_assert(TW % 4 == 0 && TH % RB == 0, "tile shape");
     static constexpr int SU = UR * US;
     static constexpr int SPHI = PH * PW;
     // shared layout (floats): u | phi[F] | taps[2][F*KP] | tab[2][F*tab_stride]
     static size_t smem_bytes(int tab_stride) {
-        return sizeof(float) * (size_t)(SU + kF * SPHI + 2 * kF * KP + 2 * kF * tab_stride);
+        return sizeof(float) * (size_t)(SU + F * SPHI + 2 * F * KP + 2 * F * tab_stride);
     }
 };
 
-template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST>
-#ifndef TNRD_MINB
-#define TNRD_MINB (768 / NT)
-#endif
-__global__ void __launch_bounds__(NT, TNRD_MINB) stage_kernel(const StageArgs p) {
-    using C = StageCfg<MS, TH, TW, RF, RB, NT>;
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB>
+__global__ void __launch_bounds__(NT, MINB) stage_kernel(const StageArgs p) {
+    using C = StageCfg<MS, TH, TW, RF, RB, NT, F>;
     constexpr int R = C::R;
     extern __shared__ __align__(16) float smem[];
     float* sU = smem;
     float* sPhi = sU + C::SU;
-    float* sTap = sPhi + kF * C::SPHI;
-    float* sTab = sTap + 2 * kF * C::KP;
-    const int tabsz = kF * p.tab_stride;
+    float* sTap = sPhi + F * C::SPHI;
+    float* sTab = sTap + 2 * F * C::KP;
+    const int tabsz = F * p.tab_stride;
 
     const int tid = threadIdx.x;
     const int img = blockIdx.z;
@@ -215,9 +214,9 @@ __global__ void __launch_bounds__(NT, TNRD_MINB) stage_kernel(const StageArgs p)
 
     // prefetch group 0 parameters
     auto prefetch = [&](int g, int buf) {
-        const float* gt = p.taps + (size_t)g * kF * C::KP;
-        float* st = sTap + buf * kF * C::KP;
-        for (int i = tid; i < kF * C::KP / 4; i += NT) cp_async16(st + 4 * i, gt + 4 * i);
+        const float* gt = p.taps + (size_t)g * F * C::KP;
+        float* st = sTap + buf * F * C::KP;
+        for (int i = tid; i < F * C::KP / 4; i += NT) cp_async16(st + 4 * i, gt + 4 * i);
         const float* gb = p.tab + (size_t)g * tabsz;
         float* sb = sTab + buf * tabsz;
         for (int i = tid; i < tabsz / 4; i += NT) cp_async16(sb + 4 * i, gb + 4 * i);
@@ -261,16 +260,13 @@ __global__ void __launch_bounds__(NT, TNRD_MINB) stage_kernel(const StageArgs p)
         cp_async_wait_all();
         __syncthreads();  // params of group g landed; previous bwd done with sPhi
         if (g + 1 < p.ngroups) prefetch(g + 1, buf ^ 1);
-        const float* tapg = sTap + buf * kF * C::KP;
+        const float* tapg = sTap + buf * F * C::KP;
         const float* tabg = sTab + buf * tabsz;
 
         // ---- forward: z = conv(u, k) on the phi region, phi = rbf(z) --------
-        for (int it = tid; it < C::FWD_ITEMS; it += NT) {
-            const int bx = it % C::NBX;
-            const int rest = it / C::NBX;
-            const int by = rest % C::NBY;
-            const int fi = rest / C::NBY;
-            const int x0 = bx * 4, y0 = by * RF;
+        // TPF threads per filter, each with the filter's taps in registers
+        {
+            const int fi = tid / C::TPF;
             float k[C::KK];
             {
                 const float4* t4 = reinterpret_cast<const float4*>(tapg + fi * C::KP);
@@ -283,51 +279,57 @@ __global__ void __launch_bounds__(NT, TNRD_MINB) stage_kernel(const StageArgs p)
                     if (4 * q + 3 < C::KK) k[4 * q + 3] = v.w;
                 }
             }
-            float acc[RF][4];
+            const float* tabf = tabg + fi * p.tab_stride;
+            float* phif = sPhi + fi * C::SPHI;
+            for (int blk = tid - fi * C::TPF; blk < C::NBLK; blk += C::TPF) {
+                const int by = blk / C::NBX;
+                const int bx = blk - by * C::NBX;
+                const int x0 = bx * 4, y0 = by * RF;
+                float acc[RF][4];
 #pragma unroll
-            for (int r = 0; r < RF; ++r)
+                for (int r = 0; r < RF; ++r)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
+                    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
 #pragma unroll
-            for (int rr = 0; rr < RF + 2 * R; ++rr) {
-                float v[4 * C::NV];
-                const float4* src = reinterpret_cast<const float4*>(sU + (y0 + rr) * C::US + x0);
+                for (int rr = 0; rr < RF + 2 * R; ++rr) {
+                    float v[4 * C::NV];
+                    const float* src = sU + (y0 + rr) * C::US + x0;
 #pragma unroll
-                for (int q = 0; q < C::NV; ++q) {
-                    const float4 t = src[q];
-                    v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
-                }
+                    for (int q = 0; q < C::NV; ++q) {
+                        const float4 t = lds128(src + 4 * q);
+                        v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+                    }
 #pragma unroll
-                for (int a = 0; a < MS; ++a) {
-                    const int ro = rr - a;
-                    if (ro >= 0 && ro < RF) {
+                    for (int a = 0; a < MS; ++a) {
+                        const int ro = rr - a;
+                        if (ro >= 0 && ro < RF) {
 #pragma unroll
-                        for (int b = 0; b < MS; ++b) {
-                            // true convolution == correlation with rot180(k)
-                            const float kk = k[(MS - 1 - a) * MS + (MS - 1 - b)];
+                            for (int b = 0; b < MS; ++b) {
+                                // true convolution == correlation with rot180(k)
+                                const float kk = k[(MS - 1 - a) * MS + (MS - 1 - b)];
 #pragma unroll
-                            for (int c = 0; c < 4; ++c) acc[ro][c] = fmaf(kk, v[c + b], acc[ro][c]);
+                                for (int c = 0; c < 4; ++c) acc[ro][c] = fmaf(kk, v[c + b], acc[ro][c]);
+                            }
                         }
                     }
                 }
-            }
-            const float* tabf = tabg + fi * p.tab_stride;
-            float* dst = sPhi + fi * C::SPHI + y0 * C::PW + x0;
+                float* dst = phif + y0 * C::PW + x0;
 #pragma unroll
-            for (int r = 0; r < RF; ++r) {
-                float4 o;
-                if (FAST) {
-                    o.x = rbf_poly(acc[r][0], tabf, p);
-                    o.y = rbf_poly(acc[r][1], tabf, p);
-                    o.z = rbf_poly(acc[r][2], tabf, p);
-                    o.w = rbf_poly(acc[r][3], tabf, p);
-                } else {
-                    o.x = rbf_direct(acc[r][0], tabf, p);
-                    o.y = rbf_direct(acc[r][1], tabf, p);
-                    o.z = rbf_direct(acc[r][2], tabf, p);
-                    o.w = rbf_direct(acc[r][3], tabf, p);
+                for (int r = 0; r < RF; ++r) {
+                    float4 o;
+                    if (FAST) {
+                        o.x = rbf_poly(acc[r][0], tabf, p);
+                        o.y = rbf_poly(acc[r][1], tabf, p);
+                        o.z = rbf_poly(acc[r][2], tabf, p);
+                        o.w = rbf_poly(acc[r][3], tabf, p);
+                    } else {
+                        o.x = rbf_direct(acc[r][0], tabf, p);
+                        o.y = rbf_direct(acc[r][1], tabf, p);
+                        o.z = rbf_direct(acc[r][2], tabf, p);
+                        o.w = rbf_direct(acc[r][3], tabf, p);
+                    }
+                    *reinterpret_cast<float4*>(dst + r * C::PW) = o;
                 }
-                *reinterpret_cast<float4*>(dst + r * C::PW) = o;
             }
         }
         __syncthreads();
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(NT, TNRD_MINB) stage_kernel(const StageArgs p)
             const int full_rows = nt_ + (C::PH - h0);
             const int mid_rows = h0 - nt_;
             const int per_f = full_rows * C::PW + mid_rows * (nl_ + C::PW - w0);
-            for (int i = tid; i < kF * per_f; i += NT) {
+            for (int i = tid; i < F * per_f; i += NT) {
                 const int j = i / per_f;
                 int rem = i - j * per_f;
                 int py, px;
@@ -375,7 +377,7 @@ __global__ void __launch_bounds__(NT, TNRD_MINB) stage_kernel(const StageArgs p)
 
         // ---- backward: force += corr(phi_i, k_i) -----------------------------
 #pragma unroll 1
-        for (int fi = split; fi < kF; fi += C::NSPLIT) {
+        for (int fi = split; fi < F; fi += C::NSPLIT) {
             float k[C::KK];
             {
                 const float4* t4 = reinterpret_cast<const float4*>(tapg + fi * C::KP);
