@@ -132,6 +132,20 @@ def main(which):
              **{f"out_{i}": sd.prox_idiv(ut, fp, lam)
                 for i, lam in enumerate((0.01, 0.3, 1.0, 10.0))},
              lams=np.array([0.01, 0.3, 1.0, 10.0]))
+    if "io" in which:
+        # files written by the reference's own io.py (io.py:133-210, 32-128)
+        import specklediff.io as sdio
+        model = ref_model(5, 3, 2, 9, seed=31, betas=[0.25, -0.5])
+        model.metadata["note"] = "golden"
+        sdio.save_model(model, os.path.join(HERE, "io_model_v1.txt"))
+        img = rng.uniform(0, 300, (7, 9))
+        sdio.save_image(img, os.path.join(HERE, "io_image.fgrid"))
+        sdio.save_image(img, os.path.join(HERE, "io_image8.pgm"), peak=255.0)
+        sdio.save_image(img, os.path.join(HERE, "io_image16.pgm"), peak=1000.0)
+        save("io_arrays", img=img, pgm8=sdio.load_image(os.path.join(HERE, "io_image8.pgm")),
+             pgm16=sdio.load_image(os.path.join(HERE, "io_image16.pgm")),
+             **pack_model(model))
+        print("wrote io fixtures")
     for key in ("c1", "c2"):
         if key in which:
             cfg = synth.CONFIGS[key]
@@ -141,4 +155,4 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["small", "c1", "c2"])
+    main(sys.argv[1:] or ["small", "io", "c1", "c2"])
