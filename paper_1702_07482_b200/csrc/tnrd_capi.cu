@@ -20,6 +20,7 @@
 #include "../../include/tnrd.h"
 #include "tnrd_stage.cuh"
 #include "tnrd_stage_tc.cuh"
+#include "tnrd_stage_tc3.cuh"
 
 using namespace tnrd;
 
@@ -89,11 +90,12 @@ struct tnrd_model {
 
 // 0 = auto (the faster kernel as measured on B200: currently
 // the CUDA-core kernel), 1 = CUDA-core only, 2 = tensor-core required,
-// 3 / 4 = CUDA-core with small / large tiles forced (tests)
+// 3 / 4 = CUDA-core with small / large tiles forced (tests), 5 = the
+// phase-locked tcgen05 kernel (tnrd_stage_tc.cuh, kept for comparison)
 static std::atomic<int> g_kernel_mode{0};
 
 extern "C" int tnrd_set_stage_kernel(int mode) {
-    if (mode < 0 || mode > 4) return fail(TNRD_EINVAL, "stage kernel mode must be in 0..4");
+    if (mode < 0 || mode > 5) return fail(TNRD_EINVAL, "stage kernel mode must be in 0..5");
     g_kernel_mode.store(mode);
     return TNRD_OK;
 }
@@ -360,13 +362,21 @@ extern "C" int tnrd_status_decode(const uint32_t* h, int* bad_stage) {
 // spread over all 148 SMs; large tiles cut the phi-halo recompute
 // (inflation 1.48 -> 1.23) once the grid has enough tiles.
 struct SmallTile { static constexpr int TH = 32, TW = 32, RF = 2, RB = 2, NT = 256, F = 4; };
-struct LargeTile { static constexpr int TH = 64, TW = 64, RF = 2, RB = 4, NT = 256, F = 2; };
+#ifndef TNRD_LARGE_RF
+#define TNRD_LARGE_RF 5
+#endif
+#ifndef TNRD_LARGE_MINB
+#define TNRD_LARGE_MINB 2
+#endif
+struct LargeTile { static constexpr int TH = 64, TW = 64, RF = TNRD_LARGE_RF, RB = 4, NT = 256, F = 2; };
 
 template <int MS, bool FAST, class T>
 struct StageKernel {
-    static constexpr int TH = T::TH, TW = T::TW, RF = T::RF, RB = T::RB, NT = T::NT, F = T::F;
+    static constexpr int TH = T::TH, TW = T::TW, RB = T::RB, NT = T::NT, F = T::F;
+    // m = 9 keeps 81 taps in registers: deeper forward blocking would spill
+    static constexpr int RF = MS >= 9 ? 2 : T::RF;
     // 3 CTAs/SM fit the register file for m <= 7; m = 9 keeps 81 taps live
-    static constexpr int MINB = std::is_same<T, LargeTile>::value ? 2 : (MS >= 9 ? 2 : 3);
+    static constexpr int MINB = std::is_same<T, LargeTile>::value ? TNRD_LARGE_MINB : (MS >= 9 ? 2 : 3);
     using C = StageCfg<MS, TH, TW, RF, RB, NT, F>;
 
     static int launch(const StageArgs& a, int batch, cudaStream_t s) {
@@ -448,6 +458,54 @@ struct StageKernelTC {
     }
 };
 
+template <int MS>
+struct StageKernelTC3 {
+    using C = tc3::Cfg<MS>;
+    static bool fits(int tab_stride) { return C::smem_bytes(tab_stride) <= 227 * 1024; }
+    static int launch(const StageArgs& a, const float* bop, int batch, cudaStream_t s) {
+        static std::mutex mu;
+        static uint64_t attr_set = 0;
+        const size_t smem = C::smem_bytes(a.tab_stride);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        auto kern = tc3::stage_kernel_tc3<MS>;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (!(attr_set & (1ull << (dev & 63)))) {
+                CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              227 * 1024));
+                attr_set |= 1ull << (dev & 63);
+            }
+        }
+        dim3 grid((a.W + C::TW - 1) / C::TW, (a.H + C::TH - 1) / C::TH, batch);
+        kern<<<grid, tc3::kNT, smem, s>>>(a, bop);
+        CUDA_TRY(cudaGetLastError());
+        g_launches.fetch_add(1);
+        return TNRD_OK;
+    }
+};
+
+static bool tc3_supported(const tnrd_model* md) {
+    if (!md->fast || !md->d_bop) return false;
+    switch (md->m) {
+        case 3: return StageKernelTC3<3>::fits(md->tab_stride);
+        case 5: return StageKernelTC3<5>::fits(md->tab_stride);
+        case 7: return StageKernelTC3<7>::fits(md->tab_stride);
+        default: return false;
+    }
+}
+
+static int dispatch_tc3(const tnrd_model* md, int t, StageArgs a, int batch, cudaStream_t s) {
+    a.ngroups = md->nk_pad / tc::kG;
+    const float* bop = md->d_bop + (size_t)t * md->bop_stage;
+    switch (md->m) {
+        case 3: return StageKernelTC3<3>::launch(a, bop, batch, s);
+        case 5: return StageKernelTC3<5>::launch(a, bop, batch, s);
+        case 7: return StageKernelTC3<7>::launch(a, bop, batch, s);
+        default: return fail(TNRD_EUNSUPPORTED, "no tensor-core stage kernel for m=%d", md->m);
+    }
+}
+
 static bool tc_supported(const tnrd_model* md) {
     if (!md->fast || !md->d_bop) return false;
     switch (md->m) {
@@ -514,8 +572,10 @@ static int launch_stage(const tnrd_model* md, int t, const float* u_in, const fl
     a.stage = t;
     a.status = d_status;
     const int mode = g_kernel_mode.load();
-    if (mode == 2 && tc_supported(md)) return dispatch_tc(md, t, a, batch, s);
-    if (mode == 2) return fail(TNRD_EUNSUPPORTED, "tensor-core stage kernel unavailable for this model");
+    if (mode == 2 && tc3_supported(md)) return dispatch_tc3(md, t, a, batch, s);
+    if (mode == 5 && tc_supported(md)) return dispatch_tc(md, t, a, batch, s);
+    if (mode == 2 || mode == 5)
+        return fail(TNRD_EUNSUPPORTED, "tensor-core stage kernel unavailable for this model");
     return md->fast ? dispatch_m<true>(md->m, a, batch, s) : dispatch_m<false>(md->m, a, batch, s);
 }
 
