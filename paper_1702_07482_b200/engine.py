@@ -280,25 +280,39 @@ def model_kernels(model, stages: Sequence | None = None) -> np.ndarray:
     return np.stack([s.kernels(model.basis, model.filter_size) for s in stages])
 
 
+_CACHE: "dict[tuple, DeviceModel]" = {}
+_CACHE_MAX = 16
+_CACHE_LOCK = threading.Lock()
+
+
+def cached_device_model(kernels, weights, lams, grid) -> DeviceModel:
+    """DeviceModel for explicit float64 parameter arrays, cached process-wide
+    by (device, fingerprint of every parameter) so in-place edits of
+    StageParams (as the reference's tests do) are seen and unchanged models
+    are uploaded once."""
+    require_cuda()
+    kernels = np.ascontiguousarray(kernels, dtype=np.float64)
+    weights = np.ascontiguousarray(weights, dtype=np.float64)
+    lams = np.ascontiguousarray(lams, dtype=np.float64)
+    dev = torch().cuda.current_device()
+    key = (dev, params_fingerprint(kernels.shape[-1], kernels, weights, lams, grid))
+    with _CACHE_LOCK:
+        dm = _CACHE.pop(key, None)
+        if dm is None:
+            while len(_CACHE) >= _CACHE_MAX:
+                _CACHE.pop(next(iter(_CACHE)))  # freed by __del__ once unreferenced
+            dm = DeviceModel(kernels, weights, lams, grid, device=dev)
+        _CACHE[key] = dm  # most recently used last
+    return dm
+
+
 def device_model_for(model, stages: Sequence | None = None,
                      kernels: np.ndarray | None = None) -> DeviceModel:
     """Cached DeviceModel for ``model`` (or for the given stage list /
-    explicit kernels).  The cache key fingerprints every parameter, so
-    in-place edits of StageParams (as the reference's tests do) are seen."""
-    require_cuda()
-    t = torch()
+    explicit (T, nk, m, m) kernels), see cached_device_model."""
     stages = list(model.stages if stages is None else stages)
     k = model_kernels(model, stages) if kernels is None else kernels
     w = np.stack([np.asarray(s.weights, dtype=np.float64) for s in stages])
     lams = np.array([math.exp(float(s.beta)) for s in stages])
     g = model.rbf
-    grid = rbf_grid_params(g.count, g.radius, g.bandwidth)
-    dev = t.cuda.current_device()
-    key = (dev, params_fingerprint(model.filter_size, k, w, lams, grid))
-    cache = model.__dict__.setdefault("_tnrd_device_cache", {})
-    dm = cache.get(key)
-    if dm is None:
-        if len(cache) >= 8:
-            cache.pop(next(iter(cache))).close()
-        dm = cache[key] = DeviceModel(k, w, lams, grid, device=dev)
-    return dm
+    return cached_device_model(k, w, lams, rbf_grid_params(g.count, g.radius, g.bandwidth))

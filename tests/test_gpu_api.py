@@ -241,3 +241,25 @@ def test_launch_counter_counts_stages(cuda):
     _lib.launch_count_reset()
     tn.run_diffusion(f, model)
     assert _lib.launch_count() == 4
+
+
+def test_plan_graph_replay_matches_eager(cuda):
+    """Plans replay a captured CUDA graph from the second call on: results
+    must be bit-identical to the eager first call, errors still reported,
+    and each call still counts T stage launches."""
+    model = synth.make_model(7, 8, 4, 63, seed=21)
+    f = np.random.default_rng(4).uniform(1, 255, (37, 45))
+    outs = []
+    for _ in range(4):
+        _lib.launch_count_reset()
+        u, _ = tn.run_diffusion(f, model)
+        assert _lib.launch_count() == 4
+        outs.append(u)
+    for u in outs[1:]:
+        np.testing.assert_array_equal(u, outs[0])
+    bad = f.copy()
+    bad[3, 4] = -1.0
+    dm = tn.device_model_for(model)
+    with pytest.raises(ValueError, match="nonnegative"):
+        dm.despeckle_host(bad.astype(np.float32))   # graph path, device-side check
+    np.testing.assert_array_equal(tn.run_diffusion(f, model)[0], outs[0])
