@@ -55,6 +55,10 @@ extern "C" {
 #define TNRD_STAGE_BOTTOM_HALO 0x4u  /* rows H..H+2r-1 of u_in are real halo rows */
 #define TNRD_STAGE_FORCE 0x8u        /* write the diffusion force instead of the prox output */
 #define TNRD_STAGE_CHECK_F 0x10u     /* validate f (finite, >= 0) -> status flags */
+#define TNRD_STAGE_PROJECTED 0x20u   /* projected-variant reaction (set from the model's variant) */
+
+#define TNRD_VARIANT_PROX 0
+#define TNRD_VARIANT_PROJECTED 1
 
 /* status block: 2 x uint32 in device memory, reset to 0xFF bytes */
 #define TNRD_STATUS_WORDS 2
@@ -77,6 +81,11 @@ int tnrd_model_create(int m, int nk, int T, int M, const double* kernels,
                       double gamma, const double* lam, int device,
                       tnrd_model** out);
 int tnrd_model_destroy(tnrd_model* model);
+/* Part of construction (call before sharing the handle): select the reaction
+ * step -- TNRD_VARIANT_PROX (default, diffusion.py:184-194) or
+ * TNRD_VARIANT_PROJECTED with its floor (diffusion.py:197-224: u_0 =
+ * max(f, floor), u' = smooth_max(u - force - lam (1/u - f^2/u^3), floor)). */
+int tnrd_model_set_variant(tnrd_model* model, int variant, double floor);
 /* m, nk, T, M, rbf path (1 = piecewise-polynomial table, 0 = direct
  * all-centre sum) */
 int tnrd_model_info(const tnrd_model* model, int* m, int* nk, int* T, int* M,

@@ -54,6 +54,11 @@ def lib():
             _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
             ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, ctypes.c_double, _dp,
             _dp, ctypes.c_int]
+        L.oracle_run_diffusion_ex.restype = ctypes.c_int
+        L.oracle_run_diffusion_ex.argtypes = [
+            _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+            ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, ctypes.c_double, _dp,
+            ctypes.c_int, ctypes.c_double, _dp, ctypes.c_int]
         L.oracle_stage.restype = None
         L.oracle_stage.argtypes = [
             _dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -139,9 +144,11 @@ def set_threads(n: int) -> None:
 
 
 def run_diffusion_arrays(f, kernels, weights, centers, gamma, lams,
-                         nthreads: int = 0):
+                         nthreads: int = 0, variant: str = "prox",
+                         floor: float = 1.0):
     """Returns (u_T float64, bad_stage) -- bad_stage is -1 when every stage
-    stayed finite (diffusion.py:238-239 semantics)."""
+    stayed finite (diffusion.py:238-239 semantics).  variant "projected"
+    follows diffusion.py:149-168, 197-224."""
     f = _c64(f)
     if f.ndim != 2:
         raise ValueError("f must be 2D")
@@ -152,9 +159,10 @@ def run_diffusion_arrays(f, kernels, weights, centers, gamma, lams,
     lams = _c64(lams)
     H, W = f.shape
     out = np.empty_like(f)
-    bad = lib().oracle_run_diffusion(
+    bad = lib().oracle_run_diffusion_ex(
         _p(f), H, W, m, nk, T, centers.size, _p(kernels), _p(weights),
-        _p(centers), float(gamma), _p(lams), _p(out), int(nthreads))
+        _p(centers), float(gamma), _p(lams), 1 if variant == "projected" else 0,
+        float(floor), _p(out), int(nthreads))
     return out, int(bad)
 
 
@@ -166,7 +174,8 @@ def run_diffusion(f, model, nthreads: int = 0) -> np.ndarray:
         raise ValueError("observation must be nonnegative")
     out, bad = run_diffusion_arrays(f, a["kernels"], a["weights"],
                                     a["centers"], a["gamma"], a["lams"],
-                                    nthreads)
+                                    nthreads, getattr(model, "variant", "prox"),
+                                    float(getattr(model, "floor", 1.0)))
     if bad >= 0:
         raise FloatingPointError(f"non-finite image after stage {bad}")
     return out

@@ -178,22 +178,58 @@ void oracle_stage(const double* u, const double* f, int H, int W, int m,
     free(force);
 }
 
+/* diffusion.py:149-156, 197-216 (projected comparison variant) */
+void oracle_stage_projected(const double* u, const double* f, int H, int W, int m,
+                            int nk, int M, const double* kernels, const double* weights,
+                            const double* centers, double gamma, double lam,
+                            double floor_, double* u_next) {
+    const size_t n = (size_t)H * W;
+    const double tau = 0.01 * floor_; /* PROJECTION_KNEE, diffusion.py:24 */
+    oracle_force(u, H, W, m, nk, M, kernels, weights, centers, gamma, u_next);
+    for (size_t p = 0; p < n; ++p) {
+        const double ut = u[p] - u_next[p] - lam * (1.0 / u[p] - f[p] * f[p] / (u[p] * u[p] * u[p]));
+        const double x = (ut - floor_) / tau;   /* logaddexp(0, x) */
+        u_next[p] = floor_ + tau * ((x > 0 ? x : 0.0) + log1p(exp(-fabs(x))));
+    }
+}
+
+int oracle_run_diffusion_ex(const double* f, int H, int W, int m, int nk, int T,
+                            int M, const double* kernels, const double* weights,
+                            const double* centers, double gamma,
+                            const double* lam, int variant, double floor_,
+                            double* u_out, int nthreads);
+
 /* diffusion.py:219-242.  Returns -1 on success, else the first stage index
  * whose output is non-finite (the reference raises FloatingPointError). */
 int oracle_run_diffusion(const double* f, int H, int W, int m, int nk, int T,
                          int M, const double* kernels, const double* weights,
                          const double* centers, double gamma,
                          const double* lam, double* u_out, int nthreads) {
+    return oracle_run_diffusion_ex(f, H, W, m, nk, T, M, kernels, weights, centers,
+                                   gamma, lam, 0, 1.0, u_out, nthreads);
+}
+
+int oracle_run_diffusion_ex(const double* f, int H, int W, int m, int nk, int T,
+                            int M, const double* kernels, const double* weights,
+                            const double* centers, double gamma,
+                            const double* lam, int variant, double floor_,
+                            double* u_out, int nthreads) {
     if (nthreads != 0) oracle_set_threads(nthreads);
     const size_t n = (size_t)H * W;
     double* u = (double*)malloc(n * sizeof(double));
+    const double u0f = variant ? floor_ : ORACLE_F_FLOOR; /* diffusion.py:219-224 */
     for (size_t p = 0; p < n; ++p)
-        u[p] = f[p] > ORACLE_F_FLOOR ? f[p] : ORACLE_F_FLOOR;
+        u[p] = f[p] > u0f ? f[p] : u0f;
     int bad = -1;
     for (int t = 0; t < T; ++t) {
-        oracle_stage(u, f, H, W, m, nk, M, kernels + (size_t)t * nk * m * m,
-                     weights + (size_t)t * nk * M, centers, gamma, lam[t],
-                     u_out);
+        if (variant)
+            oracle_stage_projected(u, f, H, W, m, nk, M, kernels + (size_t)t * nk * m * m,
+                                   weights + (size_t)t * nk * M, centers, gamma, lam[t],
+                                   floor_, u_out);
+        else
+            oracle_stage(u, f, H, W, m, nk, M, kernels + (size_t)t * nk * m * m,
+                         weights + (size_t)t * nk * M, centers, gamma, lam[t],
+                         u_out);
         for (size_t p = 0; p < n; ++p) {
             if (!isfinite(u_out[p])) { bad = t; break; }
         }

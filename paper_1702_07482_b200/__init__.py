@@ -8,7 +8,8 @@ executed as one fused sm_100a CUDA kernel through a C ABI
 from .diffusion import (VARIANTS, DiffusionModel, StageParams, StageTrace,
                         default_rbf_grid, diffusion_force, diffusion_step,
                         diffusion_step_projected, initial_state,
-                        run_diffusion, run_diffusion_batch, zero_mean_basis)
+                        projection_reaction, run_diffusion, run_diffusion_batch,
+                        smooth_max, zero_mean_basis)
 from .engine import DeviceModel, device_model_for
 from .imageops import as_image, as_kernel, conv2d, rotate180
 from .influence import RbfGrid
@@ -19,7 +20,8 @@ __all__ = [
     "VARIANTS", "DiffusionModel", "StageParams", "StageTrace",
     "default_rbf_grid", "diffusion_force", "diffusion_step",
     "diffusion_step_projected", "initial_state", "run_diffusion",
-    "run_diffusion_batch", "zero_mean_basis", "DeviceModel",
+    "run_diffusion_batch", "zero_mean_basis", "smooth_max", "projection_reaction",
+    "DeviceModel",
     "device_model_for", "as_image", "as_kernel", "conv2d", "rotate180",
     "RbfGrid", "F_FLOOR", "NoisyPair", "SpeckleConfig", "prox_idiv",
     "sample_speckle", "speckle_field",

@@ -25,6 +25,8 @@ STAGE_TOP_HALO = 0x2
 STAGE_BOTTOM_HALO = 0x4
 STAGE_FORCE = 0x8
 STAGE_CHECK_F = 0x10
+STAGE_PROJECTED = 0x20
+VARIANT_PROX, VARIANT_PROJECTED = 0, 1
 
 STATUS_WORDS = 2
 
@@ -44,6 +46,7 @@ SIGNATURES = {
                                    _c_dbl, _c_dbl, _c_dbl, _dp, _c_int,
                                    ctypes.POINTER(_vp)]),
     "tnrd_model_destroy": (_c_int, [_vp]),
+    "tnrd_model_set_variant": (_c_int, [_vp, _c_int, _c_dbl]),
     "tnrd_model_info": (_c_int, [_vp] + [ctypes.POINTER(_c_int)] * 5),
     "tnrd_model_rbf_fit": (_c_int, [_vp, ctypes.POINTER(_c_dbl),
                                     ctypes.POINTER(_c_dbl),

@@ -80,6 +80,8 @@ struct tnrd_model {
     double fit_err32 = 0;   // same with the fp32 coefficients
     double fit_scale = 0;   // max sum_j |w_ij|
     std::vector<double> lam;
+    int variant = 0;          // 0 prox, 1 projected (tnrd_model_set_variant)
+    double floor = 1.0;       // projection floor
     float* d_taps = nullptr;  // T * nk_pad * kp
     float* d_tab = nullptr;   // T * nk_pad * tab_stride
     // tensor-core forward GEMM operand (m in {3,5,7}): per stage
@@ -329,6 +331,17 @@ extern "C" int tnrd_model_rbf_fit(const tnrd_model* md, double* max_abs_err,
     return TNRD_OK;
 }
 
+extern "C" int tnrd_model_set_variant(tnrd_model* md, int variant, double floor) {
+    if (!md) return fail(TNRD_EINVAL, "model is NULL");
+    if (variant != TNRD_VARIANT_PROX && variant != TNRD_VARIANT_PROJECTED)
+        return fail(TNRD_EINVAL, "unknown variant %d", variant);
+    if (variant == TNRD_VARIANT_PROJECTED && !(floor > 0) )
+        return fail(TNRD_EINVAL, "projection floor must be positive");
+    md->variant = variant;
+    md->floor = floor;
+    return TNRD_OK;
+}
+
 extern "C" int tnrd_model_info(const tnrd_model* md, int* m, int* nk, int* T, int* M, int* fast) {
     if (!md) return fail(TNRD_EINVAL, "model is NULL");
     if (m) *m = md->m;
@@ -574,6 +587,12 @@ static int launch_stage(const tnrd_model* md, int t, const float* u_in, const fl
     a.cE = (float)(-L2E / (2.0 * md->gamma * md->gamma));
     a.mu0 = (float)md->mu0;
     a.M = md->M;
+    a.lam = (float)lam;
+    a.pfloor = (float)md->floor;
+    a.tau = (float)(0.01 * md->floor);       // PROJECTION_KNEE (diffusion.py:24)
+    a.inv_tau = (float)(1.0 / (0.01 * md->floor));
+    a.u0_floor = md->variant == TNRD_VARIANT_PROJECTED ? (float)md->floor : kFFloor;
+    if (md->variant == TNRD_VARIANT_PROJECTED) flags |= TNRD_STAGE_PROJECTED;
     a.flags = flags;
     a.stage = t;
     a.status = d_status;

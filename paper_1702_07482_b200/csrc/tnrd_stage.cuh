@@ -79,6 +79,12 @@ struct StageArgs {
     float cE;            // -log2(e) / (2 gamma^2)
     float mu0;
     int M;
+    // projected comparison variant (diffusion.py:149-168, 197-224)
+    float lam;           // lambda of the stage
+    float pfloor;        // projection floor
+    float tau;           // PROJECTION_KNEE * floor
+    float inv_tau;
+    float u0_floor;      // initial_state floor: 1e-6 (prox) or the projection floor
     uint32_t flags;
     int stage;
     uint32_t* status;    // [0] first non-finite stage (atomicMin), [1] f flags (atomicAnd ~bit)
@@ -111,6 +117,24 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// Reaction step of one pixel: the I-divergence prox (speckle.py:111-121,
+// cancellation-free for u~ < 0) or, with TNRD_STAGE_PROJECTED, the projected
+// comparison variant u' = smooth_max(u - force - lam (1/u - f^2/u^3), floor)
+// with smooth_max(x, c) = c + tau log(1 + exp((x - c)/tau)), tau = 0.01 c
+// (diffusion.py:149-168, 197-216).  `fv` is the raw observation.
+__device__ __forceinline__ float reaction(float u, float force, float fv, const StageArgs& p) {
+    if (p.flags & 0x20u) {
+        const float ut = u - force - p.lam * (1.0f / u - (fv * fv) / (u * u * u));
+        const float x = (ut - p.pfloor) * p.inv_tau;
+        return fmaf(p.tau, fmaxf(x, 0.0f) + log1pf(expf(-fabsf(x))), p.pfloor);
+    }
+    const float ff = fmaxf(fv, kFFloor);
+    const float ut = u - force;
+    const float fl2 = ff * ff;
+    const float root = sqrtf(fmaf(ut, ut, p.c8 * fl2));
+    return ut >= 0.0f ? (ut + root) * p.inv2a : (p.lam4 * fl2) / (root - ut);
+}
 
 // Half-sample symmetric reflection (np.pad mode="symmetric", one fold) and
 // clamp: positions further out than one fold only feed discarded outputs.
@@ -234,7 +258,7 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const StageArgs p) {
             if (Y < 0) Y = top_halo ? max(Y, -2 * R) : mirror_clamp(Y, p.H);
             else if (Y >= p.H) Y = bot_halo ? min(Y, p.H - 1 + 2 * R) : mirror_clamp(Y, p.H);
             float v = __ldg(uin + (int64_t)Y * p.ld + X);
-            if (floor_in) v = fmaxf(v, kFFloor);
+            if (floor_in) v = fmaxf(v, p.u0_floor);
             sU[i] = v;
         }
     }
@@ -461,12 +485,7 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const StageArgs p) {
                     if (!isfinite(fv)) fbits |= 0x1u;
                     else if (fv < 0.0f) fbits |= 0x2u;
                 }
-                const float ff = fmaxf(fv, kFFloor);
-                const float ut = u - force[r][c];
-                const float fl2 = ff * ff;
-                const float root = sqrtf(fmaf(ut, ut, p.c8 * fl2));
-                // (ut + root)/(2a), cancellation-free for ut < 0
-                res = ut >= 0.0f ? (ut + root) * p.inv2a : (p.lam4 * fl2) / (root - ut);
+                res = reaction(u, force[r][c], fv, p);
             }
             if (!isfinite(res)) bad = true;
             uout[(int64_t)Y * p.ld + X] = res;

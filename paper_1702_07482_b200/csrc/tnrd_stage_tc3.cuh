@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc3(const StageArgs p, co
             if (Y < 0) Y = top_halo ? max(Y, -2 * R) : mirror_clamp(Y, p.H);
             else if (Y >= p.H) Y = bot_halo ? min(Y, p.H - 1 + 2 * R) : mirror_clamp(Y, p.H);
             float v = __ldg(uin + (int64_t)Y * p.ld + X);
-            if (floor_in) v = fmaxf(v, kFFloor);
+            if (floor_in) v = fmaxf(v, p.u0_floor);
             sU[i] = v;
         }
     }
@@ -398,17 +398,13 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc3(const StageArgs p, co
                         res = force[r][c];
                     } else {
                         float u = __ldg(uin + (int64_t)Y * p.ld + X);
-                        if (p.flags & 0x1u) u = fmaxf(u, kFFloor);
+                        if (p.flags & 0x1u) u = fmaxf(u, p.u0_floor);
                         const float fv = __ldg(fin + (int64_t)Y * p.ld + X);
                         if (check_f) {
                             if (!isfinite(fv)) fbits |= 0x1u;
                             else if (fv < 0.0f) fbits |= 0x2u;
                         }
-                        const float ff = fmaxf(fv, kFFloor);
-                        const float ut = u - force[r][c];
-                        const float fl2 = ff * ff;
-                        const float root = sqrtf(fmaf(ut, ut, p.c8 * fl2));
-                        res = ut >= 0.0f ? (ut + root) * p.inv2a : (p.lam4 * fl2) / (root - ut);
+                        res = reaction(u, force[r][c], fv, p);
                     }
                     if (!isfinite(res)) bad = true;
                     uout[(int64_t)Y * p.ld + X] = res;

@@ -90,7 +90,8 @@ class DeviceModel:
     lams (T,) with lambda = exp(beta) (diffusion.py:72-74).
     """
 
-    def __init__(self, kernels, weights, lams, grid, device=None):
+    def __init__(self, kernels, weights, lams, grid, device=None, variant: int = 0,
+                 floor: float = 1.0):
         require_cuda()
         t = torch()
         L = _lib.load()
@@ -115,6 +116,9 @@ class DeviceModel:
                                        mu0, delta, gamma, _lib.dptr(lm),
                                        self.device.index, ctypes.byref(h)))
         self.handle = h
+        self.variant, self.floor = int(variant), float(floor)
+        if self.variant != _lib.VARIANT_PROX:
+            _lib.check(L.tnrd_model_set_variant(h, self.variant, self.floor))
         fast = ctypes.c_int(0)
         _lib.check(L.tnrd_model_info(h, None, None, None, None,
                                      ctypes.byref(fast)))
@@ -285,7 +289,8 @@ _CACHE_MAX = 16
 _CACHE_LOCK = threading.Lock()
 
 
-def cached_device_model(kernels, weights, lams, grid) -> DeviceModel:
+def cached_device_model(kernels, weights, lams, grid, variant: int = 0,
+                        floor: float = 1.0) -> DeviceModel:
     """DeviceModel for explicit float64 parameter arrays, cached process-wide
     by (device, fingerprint of every parameter) so in-place edits of
     StageParams (as the reference's tests do) are seen and unchanged models
@@ -295,13 +300,15 @@ def cached_device_model(kernels, weights, lams, grid) -> DeviceModel:
     weights = np.ascontiguousarray(weights, dtype=np.float64)
     lams = np.ascontiguousarray(lams, dtype=np.float64)
     dev = torch().cuda.current_device()
-    key = (dev, params_fingerprint(kernels.shape[-1], kernels, weights, lams, grid))
+    key = (dev, int(variant), float(floor),
+           params_fingerprint(kernels.shape[-1], kernels, weights, lams, grid))
     with _CACHE_LOCK:
         dm = _CACHE.pop(key, None)
         if dm is None:
             while len(_CACHE) >= _CACHE_MAX:
                 _CACHE.pop(next(iter(_CACHE)))  # freed by __del__ once unreferenced
-            dm = DeviceModel(kernels, weights, lams, grid, device=dev)
+            dm = DeviceModel(kernels, weights, lams, grid, device=dev, variant=variant,
+                             floor=floor)
         _CACHE[key] = dm  # most recently used last
     return dm
 
@@ -315,4 +322,7 @@ def device_model_for(model, stages: Sequence | None = None,
     w = np.stack([np.asarray(s.weights, dtype=np.float64) for s in stages])
     lams = np.array([math.exp(float(s.beta)) for s in stages])
     g = model.rbf
-    return cached_device_model(k, w, lams, rbf_grid_params(g.count, g.radius, g.bandwidth))
+    projected = getattr(model, "variant", "prox") == "projected"
+    return cached_device_model(k, w, lams, rbf_grid_params(g.count, g.radius, g.bandwidth),
+                               variant=_lib.VARIANT_PROJECTED if projected else _lib.VARIANT_PROX,
+                               floor=float(getattr(model, "floor", 1.0)))

@@ -45,8 +45,10 @@ def golden_model(g, pkg=None):
                        None if np.isnan(bw) else bw)
     stages = [pkg.StageParams(beta=float(b), coeffs=c, weights=w)
               for b, c, w in zip(g["betas"], g["coeffs"], g["weights"])]
+    variant = str(g["variant"]) if "variant" in g else "prox"
+    floor = float(g["floor"]) if "floor" in g else 1.0
     return pkg.DiffusionModel(stages=stages, filter_size=int(g["m"]), looks=1,
-                              rbf=grid)
+                              rbf=grid, variant=variant, floor=floor)
 
 
 def parity_stats(u, ref, clean=None):

@@ -32,7 +32,7 @@ CROP = 24
 
 
 def ref_model(m, nk, T, M, seed, weight_scale=0.1, beta=0.0, radius=310.0,
-              bandwidth=None, betas=None):
+              bandwidth=None, betas=None, variant="prox", floor=1.0):
     rng = np.random.default_rng(seed)
     stages = []
     for t in range(T):
@@ -42,7 +42,8 @@ def ref_model(m, nk, T, M, seed, weight_scale=0.1, beta=0.0, radius=310.0,
         b = beta if betas is None else betas[t]
         stages.append(StageParams(beta=b, coeffs=c, weights=w))
     grid = RbfGrid(count=M, radius=radius, bandwidth=bandwidth)
-    return DiffusionModel(stages=stages, filter_size=m, looks=1, rbf=grid)
+    return DiffusionModel(stages=stages, filter_size=m, looks=1, rbf=grid,
+                          variant=variant, floor=floor)
 
 
 def pack_model(model):
@@ -51,6 +52,7 @@ def pack_model(model):
         betas=np.array([s.beta for s in model.stages]),
         coeffs=np.stack([s.coeffs for s in model.stages]),
         weights=np.stack([s.weights for s in model.stages]),
+        variant=model.variant, floor=np.float64(model.floor),
         rbf_count=model.rbf.count, rbf_radius=model.rbf.radius,
         rbf_bandwidth=np.nan if model.rbf.bandwidth is None
         else model.rbf.bandwidth)
@@ -132,6 +134,15 @@ def main(which):
              **{f"out_{i}": sd.prox_idiv(ut, fp, lam)
                 for i, lam in enumerate((0.01, 0.3, 1.0, 10.0))},
              lams=np.array([0.01, 0.3, 1.0, 10.0]))
+    if "projected" in which:
+        # the comparison variant (diffusion.py:149-168, 197-224)
+        prng = np.random.default_rng(777)
+        full_case("projected_m3", prng.uniform(0, 255, (16, 16)),
+                  ref_model(3, 2, 3, 7, seed=41, weight_scale=0.2, variant="projected"))
+        full_case("projected_m7", prng.uniform(1, 255, (36, 41)),
+                  ref_model(7, 8, 3, 63, seed=42, variant="projected", betas=[0.2, -0.3, 0.5]))
+        full_case("projected_floor3", prng.uniform(0, 60, (25, 30)),
+                  ref_model(5, 6, 2, 63, seed=43, variant="projected", floor=3.0))
     if "io" in which:
         # files written by the reference's own io.py (io.py:133-210, 32-128)
         import specklediff.io as sdio
@@ -155,4 +166,4 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["small", "io", "c1", "c2"])
+    main(sys.argv[1:] or ["small", "projected", "io", "c1", "c2"])

@@ -263,3 +263,44 @@ def test_plan_graph_replay_matches_eager(cuda):
     with pytest.raises(ValueError, match="nonnegative"):
         dm.despeckle_host(bad.astype(np.float32))   # graph path, device-side check
     np.testing.assert_array_equal(tn.run_diffusion(f, model)[0], outs[0])
+
+
+# ------------------------------------------------------------- projected variant
+# reference tests/test_diffusion.py:161-204
+
+def test_projected_floor_respected(cuda):
+    rng = np.random.default_rng(9)
+    model = make_model(rng, T=3, weight_scale=0.2)
+    model.variant = "projected"
+    f = rng.uniform(0, 255, (16, 16))
+    out, _ = tn.run_diffusion(f, model)
+    assert np.all(out >= model.floor - 1e-6)
+
+
+def test_projected_step_matches_primitives(cuda, oracle):
+    rng = np.random.default_rng(11)
+    model = make_model(rng, nk=2, M=7)
+    model.variant = "projected"
+    stage = model.stages[0]
+    f = rng.uniform(1, 200, (10, 10)).astype(np.float32).astype(np.float64)
+    u = rng.uniform(2, 200, (10, 10)).astype(np.float32).astype(np.float64)
+    out, trace = tn.diffusion_step_projected(u, f, stage, model)
+    kern = stage.kernels(model.basis, model.filter_size)
+    g = model.rbf
+    force = oracle.force(u, kern, stage.weights, g.centers, g.gamma)
+    u_tilde = u - force - stage.lam * (1.0 / u - f ** 2 / u ** 3)
+    expected = tn.smooth_max(u_tilde, model.floor)
+    assert rel(out, expected) < 1e-5
+    assert np.abs(trace.u_tilde - u_tilde).max() < 1e-4 * np.abs(u_tilde).max()
+
+
+def test_projected_invalid_floor_and_smooth_max(cuda):
+    rng = np.random.default_rng(10)
+    with pytest.raises(ValueError, match="floor"):
+        tn.DiffusionModel(stages=make_model(rng).stages, filter_size=3, looks=4,
+                          variant="projected", floor=0.0)
+    c = 1.0
+    x = np.array([c + 10.0, c + 50.0])
+    assert np.abs(tn.smooth_max(x, c) - x).max() < 1e-6
+    x = np.array([c - 10.0, -50.0])
+    assert np.abs(tn.smooth_max(x, c) - c).max() < 1e-6
