@@ -387,7 +387,10 @@ struct SmallTile { static constexpr int TH = 32, TW = 32, RF = 2, RB = 2, NT = 2
 #ifndef TNRD_LARGE_MINB
 #define TNRD_LARGE_MINB 2
 #endif
-struct LargeTile { static constexpr int TH = 64, TW = 64, RF = TNRD_LARGE_RF, RB = 4, NT = 256, F = 2; };
+#ifndef TNRD_LARGE_F
+#define TNRD_LARGE_F 2
+#endif
+struct LargeTile { static constexpr int TH = 64, TW = 64, RF = TNRD_LARGE_RF, RB = 4, NT = 256, F = TNRD_LARGE_F; };
 
 template <int MS, bool FAST, class T>
 struct StageKernel {

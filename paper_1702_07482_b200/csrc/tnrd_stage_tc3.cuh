@@ -51,12 +51,14 @@ __device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity
     const long long t0 = clock64();
     for (;;) {
         uint32_t done;
+        // the suspend-time hint parks the warp in hardware until the phase
+        // flips (or ~0.5 ms pass) instead of spinning on issue slots
         asm volatile(
             "{\n\t.reg .pred P1;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, P1;\n\t}\n"
             : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(500000u)
             : "memory");
         if (done) return;
         if (clock64() - t0 > 4000000000LL) __trap();
@@ -264,18 +266,25 @@ __global__ void __launch_bounds__(kNT, 1) stage_kernel_tc3(const StageArgs p, co
             half_sync(h);                                  // taps/tables of sg landed for the half
             mbar_wait_bounded(&tmem_full[buf], (b >> 1) & 1);
             fence_after();
-            // ---- RBF: TMEM -> phi (this half's slot) ---------------------------
-#pragma unroll 1
-            for (int blk = wg * 8; blk < wg * 8 + 8; ++blk) {
-                float z[kS];
-                tmem_ld4(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * 256 + blk * kG + s * kS), z);
+            // ---- RBF: TMEM -> phi (this half's slot), 2 blocks (8 z) per pass ---
+            {
                 const int row = 32 * q + lane;
-                const int band = blk >> 3, cg = (blk >> 2) & 1, o = blk & 3;
-                const int py = 16 * band + (row >> 3);
-                const int px = 32 * cg + 4 * (row & 7) + o;
+                const uint32_t tbase = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * 256 + s * kS);
+                const int prow = (row >> 3) * kSPW + 4 * (row & 7);   // phi offset within a block
+#pragma unroll 1
+                for (int blk = wg * 8; blk < wg * 8 + 8; blk += 2) {
+                    float z[2][kS];
+                    tmem_ld4(tbase + (uint32_t)(blk * kG), z[0]);
+                    tmem_ld4(tbase + (uint32_t)((blk + 1) * kG), z[1]);
 #pragma unroll
-                for (int j = 0; j < kS; ++j)
-                    sPhi[j * C::SPHI + py * kSPW + px] = rbf_poly(z[j], sTab + j * p.tab_stride, p);
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        const int b2 = blk + h2;
+                        const int off = 16 * (b2 >> 3) * kSPW + 32 * ((b2 >> 2) & 1) + (b2 & 3) + prow;
+#pragma unroll
+                        for (int j = 0; j < kS; ++j)
+                            sPhi[j * C::SPHI + off] = rbf_poly(z[h2][j], sTab + j * p.tab_stride, p);
+                    }
+                }
             }
             fence_before();
             half_sync(h);                                  // slot complete; TMEM reads of sg done
