@@ -132,6 +132,8 @@ def dptr(a) -> _dp:
 
 KERNEL_AUTO, KERNEL_CUDA_CORE, KERNEL_TENSOR_CORE = 0, 1, 2
 KERNEL_SMALL_TILES, KERNEL_LARGE_TILES = 3, 4
+KERNEL_TC_PHASED = 5
+KERNEL_SPLIT_LARGE, KERNEL_SPLIT_SMALL = 6, 7
 
 
 def set_stage_kernel(mode: int) -> None:

@@ -12,6 +12,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <type_traits>
 #include <string>
@@ -88,16 +89,23 @@ struct tnrd_model {
     // [nk_pad/16 groups][m][ksteps][2 prec][2 kc][16][4]
     float* d_bop = nullptr;
     size_t bop_stage = 0;     // floats per stage
+    // split-kernel workspaces, one per stream (launches on one stream are
+    // ordered, so a stream's workspace is never used by two kernels at once);
+    // zero-filled at allocation and left zeroed by every split launch
+    struct SplitBuf { void* ptr = nullptr; size_t bytes = 0; };
+    mutable std::mutex ws_mu;
+    mutable std::map<cudaStream_t, SplitBuf> ws;
 };
 
 // 0 = auto (the faster kernel as measured on B200: currently
-// the CUDA-core kernel), 1 = CUDA-core only, 2 = tensor-core required,
-// 3 / 4 = CUDA-core with small / large tiles forced (tests), 5 = the
-// phase-locked tcgen05 kernel (tnrd_stage_tc.cuh, kept for comparison)
+// the CUDA-core kernels), 1 = CUDA-core only, 2 = tensor-core required,
+// 3 / 4 = CUDA-core tile kernel with small / large tiles forced (tests), 5 =
+// the phase-locked tcgen05 kernel (tnrd_stage_tc.cuh, kept for comparison),
+// 6 / 7 = CUDA-core split kernel with large / small tiles forced
 static std::atomic<int> g_kernel_mode{0};
 
 extern "C" int tnrd_set_stage_kernel(int mode) {
-    if (mode < 0 || mode > 5) return fail(TNRD_EINVAL, "stage kernel mode must be in 0..5");
+    if (mode < 0 || mode > 7) return fail(TNRD_EINVAL, "stage kernel mode must be in 0..7");
     g_kernel_mode.store(mode);
     return TNRD_OK;
 }
@@ -315,6 +323,7 @@ extern "C" int tnrd_model_destroy(tnrd_model* md) {
         cudaFree(md->d_taps);
         cudaFree(md->d_tab);
         cudaFree(md->d_bop);
+        for (auto& kv : md->ws) cudaFree(kv.second.ptr);
     }
     delete md;
     return TNRD_OK;
@@ -391,6 +400,15 @@ struct SmallTile { static constexpr int TH = 32, TW = 32, RF = 2, RB = 2, NT = 2
 #define TNRD_LARGE_F 2
 #endif
 struct LargeTile { static constexpr int TH = 64, TW = 64, RF = TNRD_LARGE_RF, RB = 4, NT = 256, F = TNRD_LARGE_F; };
+#ifndef TNRD_SPLIT_F
+#define TNRD_SPLIT_F 2
+#endif
+// split kernel units: one filter per unit halves the granularity of the SM
+// balance (a 512^2 image = 64 tiles x 48 units over 148 SMs)
+struct SplitTile { static constexpr int TH = 64, TW = 64, RF = TNRD_LARGE_RF, RB = 4, NT = 256, F = TNRD_SPLIT_F; };
+
+
+constexpr size_t kMaxSplitBytes = size_t(1) << 30;
 
 template <int MS, bool FAST, class T>
 struct StageKernel {
@@ -398,8 +416,19 @@ struct StageKernel {
     // m = 9 keeps 81 taps in registers: deeper forward blocking would spill
     static constexpr int RF = MS >= 9 ? 2 : T::RF;
     // 3 CTAs/SM fit the register file for m <= 7; m = 9 keeps 81 taps live
-    static constexpr int MINB = std::is_same<T, LargeTile>::value ? TNRD_LARGE_MINB : (MS >= 9 ? 2 : 3);
+    static constexpr int MINB = T::TH == 64 ? TNRD_LARGE_MINB : (MS >= 9 ? 2 : 3);
     using C = StageCfg<MS, TH, TW, RF, RB, NT, F>;
+
+    template <class K>
+    static int prepare(K kern, int dev, uint64_t& attr_set, std::mutex& mu) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!(attr_set & (1ull << (dev & 63)))) {
+            CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          160 * 1024));
+            attr_set |= 1ull << (dev & 63);
+        }
+        return TNRD_OK;
+    }
 
     static int launch(const StageArgs& a, int batch, cudaStream_t s) {
         static std::mutex mu;
@@ -408,14 +437,8 @@ struct StageKernel {
         int dev = 0;
         cudaGetDevice(&dev);
         auto kern = stage_kernel<MS, TH, TW, RF, RB, NT, FAST, F, MINB>;
-        {
-            std::lock_guard<std::mutex> lk(mu);
-            if (!(attr_set & (1ull << (dev & 63)))) {
-                CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              160 * 1024));
-                attr_set |= 1ull << (dev & 63);
-            }
-        }
+        int rc = prepare(kern, dev, attr_set, mu);
+        if (rc) return rc;
         dim3 grid((a.W + TW - 1) / TW, (a.H + TH - 1) / TH, batch);
         StageArgs b = a;
         b.ngroups = (a.nk + F - 1) / F;
@@ -424,13 +447,92 @@ struct StageKernel {
         g_launches.fetch_add(1);
         return TNRD_OK;
     }
+
+    static long tiles(const StageArgs& a, int batch) {
+        return (long)((a.W + TW - 1) / TW) * ((a.H + TH - 1) / TH) * batch;
+    }
+    static size_t ws_bytes(const StageArgs& a, int batch) {
+        const long nt = tiles(a, batch);
+        return (size_t)nt * ((a.nk + F - 1) / F) * TH * TW * sizeof(float);
+    }
+
+    // persistent grid of (SMs x resident CTAs) over (tile, group) units
+    static int launch_split(const StageArgs& a, int batch, void* wsp, cudaStream_t s) {
+        static std::mutex mu;
+        static uint64_t attr_set = 0;
+        static int occ[64] = {0};
+        const size_t smem = C::smem_bytes(a.tab_stride);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        auto kern = stage_kernel_split<MS, TH, TW, RF, RB, NT, FAST, F, MINB>;
+        int rc = prepare(kern, dev, attr_set, mu);
+        if (rc) return rc;
+        int per_sm = 0, sms = 0;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            per_sm = occ[dev & 63];
+            if (per_sm == 0) {
+                CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+                occ[dev & 63] = per_sm = std::max(per_sm, 1);
+            }
+        }
+        CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        StageArgs b = a;
+        b.ngroups = (a.nk + F - 1) / F;
+        SplitWs w;
+        w.tiles_x = (a.W + TW - 1) / TW;
+        w.tiles_y = (a.H + TH - 1) / TH;
+        w.tiles = w.tiles_x * w.tiles_y * batch;
+        w.part = static_cast<float*>(wsp);
+        const long units = (long)w.tiles * b.ngroups;
+        const int grid = (int)std::min<long>(units, (long)sms * per_sm);
+        kern<<<grid, NT, smem, s>>>(b, w);
+        CUDA_TRY(cudaGetLastError());
+        const long quads = (long)w.tiles * (TH * TW / 4);
+        const int rgrid = (int)std::min<long>((quads + 127) / 128, (long)sms * 16);
+        stage_reduce_kernel<TH, TW><<<rgrid, 128, 0, s>>>(b, w);
+        CUDA_TRY(cudaGetLastError());
+        g_launches.fetch_add(2);
+        return TNRD_OK;
+    }
 };
 
-// large tiles once they give >= 4 waves of 2 CTAs on 148 SMs
+// Kernel choice (measured on B200): whole large tiles once
+// the grid gives >= 3 waves of 2 CTAs per SM; below that the split kernel,
+// with large tiles when there are >= 2 units per CTA slot, else small tiles
+// (more, cheaper units: a 256^2 image).
+static int sm_count() {
+    static std::atomic<int> cached{0};
+    int n = cached.load();
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+            n = 148;
+        cached.store(n);
+    }
+    return n;
+}
+
 static bool use_large_tiles(const StageArgs& a, int batch) {
-    const long tiles = (long)((a.W + LargeTile::TW - 1) / LargeTile::TW) *
-                       ((a.H + LargeTile::TH - 1) / LargeTile::TH) * batch;
-    return tiles >= 4L * 2 * 148;
+    return StageKernel<7, true, LargeTile>::tiles(a, batch) >= 3L * 2 * sm_count();
+}
+
+static bool use_split_large(const StageArgs& a, int batch) {
+    const long units = StageKernel<7, true, SplitTile>::tiles(a, batch) * ((a.nk + SplitTile::F - 1) / SplitTile::F);
+    return units >= 2L * 2 * sm_count();
+}
+
+// tile configuration of the CUDA-core stage for this launch: 0 tile kernel
+// small tiles, 1 tile kernel large tiles, 2 split kernel large, 3 split small
+static int cc_variant(const StageArgs& a, int batch) {
+    switch (g_kernel_mode.load()) {
+        case 3: return 0;
+        case 4: return 1;
+        case 6: return 2;
+        case 7: return 3;
+        default: return use_large_tiles(a, batch) ? 1 : (use_split_large(a, batch) ? 2 : 3);
+    }
 }
 
 template <bool FAST, class T>
@@ -444,12 +546,68 @@ static int dispatch_m_t(int m, const StageArgs& a, int batch, cudaStream_t s) {
     }
 }
 
+template <bool FAST, class T>
+static size_t split_bytes_m_t(int m, const StageArgs& a, int batch) {
+    switch (m) {
+        case 3: return StageKernel<3, FAST, T>::ws_bytes(a, batch);
+        case 5: return StageKernel<5, FAST, T>::ws_bytes(a, batch);
+        case 7: return StageKernel<7, FAST, T>::ws_bytes(a, batch);
+        default: return StageKernel<9, FAST, T>::ws_bytes(a, batch);
+    }
+}
+
+template <bool FAST, class T>
+static int dispatch_split_m_t(int m, const StageArgs& a, int batch, void* ws, cudaStream_t s) {
+    switch (m) {
+        case 3: return StageKernel<3, FAST, T>::launch_split(a, batch, ws, s);
+        case 5: return StageKernel<5, FAST, T>::launch_split(a, batch, ws, s);
+        case 7: return StageKernel<7, FAST, T>::launch_split(a, batch, ws, s);
+        case 9: return StageKernel<9, FAST, T>::launch_split(a, batch, ws, s);
+        default: return fail(TNRD_EUNSUPPORTED, "unsupported filter size %d", m);
+    }
+}
+
+// the stream's split workspace, grown (zero-filled) on demand
+static int split_workspace(const tnrd_model* md, cudaStream_t s, size_t bytes, void** out) {
+    std::lock_guard<std::mutex> lk(md->ws_mu);
+    auto& b = md->ws[s];
+    if (b.bytes < bytes) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+        if (cs != cudaStreamCaptureStatusNone)
+            return fail(TNRD_ECUDA, "split workspace must be allocated before stream capture");
+        if (b.ptr) {
+            CUDA_TRY(cudaStreamSynchronize(s));
+            cudaFree(b.ptr);
+            b.ptr = nullptr;
+            b.bytes = 0;
+        }
+        CUDA_TRY(cudaMalloc(&b.ptr, bytes));
+        CUDA_TRY(cudaMemset(b.ptr, 0, bytes));
+        b.bytes = bytes;
+    }
+    *out = b.ptr;
+    return TNRD_OK;
+}
+
 template <bool FAST>
-static int dispatch_m(int m, const StageArgs& a, int batch, cudaStream_t s) {
-    const int mode = g_kernel_mode.load();
-    const bool large = mode == 4 || (mode != 3 && use_large_tiles(a, batch));
-    return large ? dispatch_m_t<FAST, LargeTile>(m, a, batch, s)
-                 : dispatch_m_t<FAST, SmallTile>(m, a, batch, s);
+static int dispatch_m(const tnrd_model* md, const StageArgs& a, int batch, cudaStream_t s) {
+    const int m = md->m;
+    const int v = cc_variant(a, batch);
+    if (v == 0) return dispatch_m_t<FAST, SmallTile>(m, a, batch, s);
+    if (v == 1) return dispatch_m_t<FAST, LargeTile>(m, a, batch, s);
+    // the split kernel's partials workspace is bounded (it only pays off on
+    // small grids anyway)
+    if ((v == 2 ? split_bytes_m_t<FAST, SplitTile>(m, a, batch)
+                : split_bytes_m_t<FAST, SmallTile>(m, a, batch)) > kMaxSplitBytes)
+        return dispatch_m_t<FAST, LargeTile>(m, a, batch, s);
+    const size_t bytes = v == 2 ? split_bytes_m_t<FAST, SplitTile>(m, a, batch)
+                                : split_bytes_m_t<FAST, SmallTile>(m, a, batch);
+    void* ws = nullptr;
+    int rc = split_workspace(md, s, bytes, &ws);
+    if (rc) return rc;
+    return v == 2 ? dispatch_split_m_t<FAST, SplitTile>(m, a, batch, ws, s)
+                  : dispatch_split_m_t<FAST, SmallTile>(m, a, batch, ws, s);
 }
 
 template <int MS>
@@ -604,7 +762,7 @@ static int launch_stage(const tnrd_model* md, int t, const float* u_in, const fl
     if (mode == 5 && tc_supported(md)) return dispatch_tc(md, t, a, batch, s);
     if (mode == 2 || mode == 5)
         return fail(TNRD_EUNSUPPORTED, "tensor-core stage kernel unavailable for this model");
-    return md->fast ? dispatch_m<true>(md->m, a, batch, s) : dispatch_m<false>(md->m, a, batch, s);
+    return md->fast ? dispatch_m<true>(md, a, batch, s) : dispatch_m<false>(md, a, batch, s);
 }
 
 extern "C" int tnrd_stage(const tnrd_model* md, int t, const float* u_in, const float* f,
@@ -655,6 +813,7 @@ struct tnrd_plan {
     // graph (status reset + T kernels) and replayed: one launch per call
     cudaGraphExec_t graph = nullptr;
     int graph_mode = -1;           // stage-kernel mode the graph was captured with
+    uint64_t graph_launches = 0;   // kernels in the graph
     long runs = 0;
 };
 
@@ -717,8 +876,14 @@ static int plan_run(tnrd_plan* p, const float* f_dev, float* u_dev) {
         const uint64_t before = g_launches.load();
         int rc = plan_eager(p, f_dev, u_dev);
         cudaError_t e = cudaStreamEndCapture(p->stream, &g);
+        const uint64_t captured = g_launches.load() - before;
         g_launches.store(before);  // captured, not launched
-        if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+        if (rc) {
+            // e.g. a workspace that must grow first: run eagerly this time
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            return plan_eager(p, f_dev, u_dev);
+        }
         if (e != cudaSuccess || cudaGraphInstantiate(&p->graph, g, 0) != cudaSuccess) {
             if (g) cudaGraphDestroy(g);
             cudaGetLastError();
@@ -727,9 +892,10 @@ static int plan_run(tnrd_plan* p, const float* f_dev, float* u_dev) {
         }
         cudaGraphDestroy(g);
         p->graph_mode = mode;
+        p->graph_launches = captured;
     }
     CUDA_TRY(cudaGraphLaunch(p->graph, p->stream));
-    g_launches.fetch_add((uint64_t)p->md->T);
+    g_launches.fetch_add(p->graph_launches);
     return TNRD_OK;
 }
 
@@ -764,6 +930,14 @@ extern "C" int tnrd_plan_despeckle_host(tnrd_plan* p, const float* f_host, float
 extern "C" void* tnrd_plan_stream(tnrd_plan* p) { return p ? (void*)p->stream : nullptr; }
 extern "C" float* tnrd_plan_f_device(tnrd_plan* p) { return p ? p->d_f : nullptr; }
 extern "C" float* tnrd_plan_u_device(tnrd_plan* p) { return p ? p->d_u : nullptr; }
+
+#ifdef TNRD_SPLIT_TRACE
+extern "C" __attribute__((visibility("default"))) int tnrd_debug_split_trace(unsigned long long* out, int n) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpyFromSymbol(out, g_split_trace, (size_t)std::min(n, 4096) * 4 * sizeof(unsigned long long)));
+    return TNRD_OK;
+}
+#endif
 
 // ----------------------------------------------------------------- conv2d / prox
 

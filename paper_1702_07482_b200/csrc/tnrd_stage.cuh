@@ -16,9 +16,9 @@
 //     are prefetched into shared memory with cp.async one group ahead;
 //   * forward pass: each work item = one filter x RF x 4 phi block; the 49
 //     taps live in registers, u rows are read as float4;
-//   * the RBF phi_i is evaluated from a per-filter piecewise degree-11
-//     polynomial table (float64 Chebyshev fit on the host, error < 1e-10 of
-//     sum|w|): 3 conflict-free LDS.128 + 11 FFMA per response instead of
+//   * the RBF phi_i is evaluated from a per-filter piecewise degree-7
+//     polynomial table (float64 Chebyshev fit on the host, error ~1e-9 of
+//     sum|w|): 2 conflict-free LDS.128 + 7 FFMA per response instead of
 //     M=63 exponentials;
 //   * phi halos that fall outside the image are filled by mirroring the
 //     in-image phi values (reference pads phi itself, diffusion.py:180);
@@ -26,7 +26,10 @@
 //     the group's filters and keeps its partial force in registers across
 //     all groups; the two halves are summed once in the epilogue;
 //   * epilogue: u~ = u - force, cancellation-free prox, non-finite flag,
-//     f validation (stage 0), store.
+//     f validation (stage 0), store;
+//   * small grids (one 512^2 image) run the split kernel instead: units of
+//     (tile, filter group) over a persistent grid, partial forces reduced in
+//     a fixed order by the tile's last unit (stage_kernel_split).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -215,6 +218,264 @@ struct StageCfg {
     }
 };
 
+// ---- building blocks shared by the tile kernel and the split kernel --------
+
+// u tile with a 2r halo, mirrored at image edges (or read from the halo rows
+// of a row strip), floored on the first stage (initial_state,
+// diffusion.py:219-224)
+template <class C, int NT>
+__device__ __forceinline__ void stage_u_tile(const StageArgs& p, float* sU, const float* __restrict__ uin,
+                                             int Y0, int X0, bool top_halo, bool bot_halo, int tid) {
+    constexpr int R = C::R;
+    constexpr int B = 8;  // loads in flight per thread
+    const bool floor_in = p.flags & 0x1u;
+    for (int i0 = tid; i0 < C::SU; i0 += B * NT) {
+        float v[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            const int i = i0 + j * NT;
+            if (i < C::SU) {
+                const int uy = i / C::US, ux = i - uy * C::US;
+                int Y = Y0 - 2 * R + uy;
+                const int X = mirror_clamp(X0 - 2 * R + ux, p.W);
+                if (Y < 0) Y = top_halo ? max(Y, -2 * R) : mirror_clamp(Y, p.H);
+                else if (Y >= p.H) Y = bot_halo ? min(Y, p.H - 1 + 2 * R) : mirror_clamp(Y, p.H);
+                v[j] = __ldg(uin + (int64_t)Y * p.ld + X);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            const int i = i0 + j * NT;
+            if (i < C::SU) sU[i] = floor_in ? fmaxf(v[j], p.u0_floor) : v[j];
+        }
+    }
+}
+
+template <class C, int F, int NT>
+__device__ __forceinline__ void prefetch_group(const StageArgs& p, float* sTap, float* sTab, int g,
+                                               int buf, int tid) {
+    const int tabsz = F * p.tab_stride;
+    const float* gt = p.taps + (size_t)g * F * C::KP;
+    float* st = sTap + buf * F * C::KP;
+    for (int i = tid; i < F * C::KP / 4; i += NT) cp_async16(st + 4 * i, gt + 4 * i);
+    const float* gb = p.tab + (size_t)g * tabsz;
+    float* sb = sTab + buf * tabsz;
+    for (int i = tid; i < tabsz / 4; i += NT) cp_async16(sb + 4 * i, gb + 4 * i);
+    cp_async_commit();
+}
+
+template <class C>
+__device__ __forceinline__ void load_taps(const float* tap, float (&k)[C::KK]) {
+    const float4* t4 = reinterpret_cast<const float4*>(tap);
+#pragma unroll
+    for (int q = 0; q < C::KP / 4; ++q) {
+        const float4 v = t4[q];
+        if (4 * q + 0 < C::KK) k[4 * q + 0] = v.x;
+        if (4 * q + 1 < C::KK) k[4 * q + 1] = v.y;
+        if (4 * q + 2 < C::KK) k[4 * q + 2] = v.z;
+        if (4 * q + 3 < C::KK) k[4 * q + 3] = v.w;
+    }
+}
+
+// forward: z = conv(u, k) on the phi region, phi = rbf(z); TPF threads per
+// filter, each with the filter's taps in registers
+template <class C, int MS, int RF, int F, bool FAST>
+__device__ __forceinline__ void forward_group(const StageArgs& p, const float* sU, float* sPhi,
+                                              const float* tapg, const float* tabg, int tid) {
+    constexpr int R = C::R;
+    const int fi = tid / C::TPF;
+    float k[C::KK];
+    load_taps<C>(tapg + fi * C::KP, k);
+    const float* tabf = tabg + fi * p.tab_stride;
+    float* phif = sPhi + fi * C::SPHI;
+    for (int blk = tid - fi * C::TPF; blk < C::NBLK; blk += C::TPF) {
+        const int by = blk / C::NBX;
+        const int bx = blk - by * C::NBX;
+        const int x0 = bx * 4, y0 = by * RF;
+        float acc[RF][4];
+#pragma unroll
+        for (int r = 0; r < RF; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
+#pragma unroll
+        for (int rr = 0; rr < RF + 2 * R; ++rr) {
+            float v[4 * C::NV];
+            const float* src = sU + (y0 + rr) * C::US + x0;
+#pragma unroll
+            for (int q = 0; q < C::NV; ++q) {
+                const float4 t = lds128(src + 4 * q);
+                v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+            }
+#pragma unroll
+            for (int a = 0; a < MS; ++a) {
+                const int ro = rr - a;
+                if (ro >= 0 && ro < RF) {
+#pragma unroll
+                    for (int b = 0; b < MS; ++b) {
+                        // true convolution == correlation with rot180(k)
+                        const float kk = k[(MS - 1 - a) * MS + (MS - 1 - b)];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) acc[ro][c] = fmaf(kk, v[c + b], acc[ro][c]);
+                    }
+                }
+            }
+        }
+        float* dst = phif + y0 * C::PW + x0;
+#pragma unroll
+        for (int r = 0; r < RF; ++r) {
+            float4 o;
+            if (FAST) {
+                o.x = rbf_poly(acc[r][0], tabf, p);
+                o.y = rbf_poly(acc[r][1], tabf, p);
+                o.z = rbf_poly(acc[r][2], tabf, p);
+                o.w = rbf_poly(acc[r][3], tabf, p);
+            } else {
+                o.x = rbf_direct(acc[r][0], tabf, p);
+                o.y = rbf_direct(acc[r][1], tabf, p);
+                o.z = rbf_direct(acc[r][2], tabf, p);
+                o.w = rbf_direct(acc[r][3], tabf, p);
+            }
+            *reinterpret_cast<float4*>(dst + r * C::PW) = o;
+        }
+    }
+}
+
+// phi halo outside the image = mirror of in-image phi (the reference pads phi
+// itself, diffusion.py:180).  Only the out-of-image band of the phi region is
+// rewritten: rows [0, nt) and [h0, PH) and, for the rows in between, columns
+// [0, nl) and [w0, PW); sources are in-image.  Ends with a CTA barrier when
+// it wrote anything (uniform condition).
+template <class C, int F, int NT, int TH, int TW>
+__device__ __forceinline__ void fix_phi(const StageArgs& p, float* sPhi, int Y0, int X0,
+                                        bool top_halo, bool bot_halo, int tid) {
+    constexpr int R = C::R;
+    const bool fix_l = X0 - R < 0;
+    const bool fix_r = X0 + TW + R > p.W;
+    const bool fix_t = !top_halo && (Y0 - R < 0);
+    const bool fix_b = !bot_halo && (Y0 + TH + R > p.H);
+    if (!(fix_l || fix_r || fix_t || fix_b)) return;
+    const int nt_ = fix_t ? min(R, C::PH) : 0;
+    const int h0 = fix_b ? max(nt_, min(C::PH, p.H - (Y0 - R))) : C::PH;
+    const int nl_ = fix_l ? R : 0;
+    const int w0 = fix_r ? max(nl_, min(C::PW, p.W - (X0 - R))) : C::PW;
+    const int full_rows = nt_ + (C::PH - h0);
+    const int mid_rows = h0 - nt_;
+    const int per_f = full_rows * C::PW + mid_rows * (nl_ + C::PW - w0);
+    for (int i = tid; i < F * per_f; i += NT) {
+        const int j = i / per_f;
+        int rem = i - j * per_f;
+        int py, px;
+        if (rem < full_rows * C::PW) {
+            const int rr = rem / C::PW;
+            px = rem - rr * C::PW;
+            py = rr < nt_ ? rr : h0 + (rr - nt_);
+        } else {
+            rem -= full_rows * C::PW;
+            const int wcols = nl_ + C::PW - w0;
+            const int rr = rem / wcols, cc = rem - rr * wcols;
+            py = nt_ + rr;
+            px = cc < nl_ ? cc : w0 + (cc - nl_);
+        }
+        const int Y = Y0 - R + py, X = X0 - R + px;
+        int sy = Y, sx = X;
+        if (X < 0 && X >= -R) sx = -1 - X;
+        else if (X >= p.W && X < p.W + R) sx = 2 * p.W - 1 - X;
+        if (!top_halo && Y < 0 && Y >= -R) sy = -1 - Y;
+        else if (!bot_halo && Y >= p.H && Y < p.H + R) sy = 2 * p.H - 1 - Y;
+        if (sy != Y || sx != X) {
+            const int spy = sy - (Y0 - R), spx = sx - (X0 - R);
+            sPhi[j * C::SPHI + py * C::PW + px] = sPhi[j * C::SPHI + spy * C::PW + spx];
+        }
+    }
+    __syncthreads();
+}
+
+// backward: force += corr(phi_i, k_i) for this thread's filters of the group
+template <class C, int MS, int RB, int F>
+__device__ __forceinline__ void backward_group(const float* sPhi, const float* tapg, int split,
+                                               int ox0, int oy0, float (&force)[RB][4]) {
+    constexpr int R = C::R;
+#pragma unroll 1
+    for (int fi = split; fi < F; fi += C::NSPLIT) {
+        float k[C::KK];
+        load_taps<C>(tapg + fi * C::KP, k);
+        const float* ph = sPhi + fi * C::SPHI;
+#pragma unroll
+        for (int rr = 0; rr < RB + 2 * R; ++rr) {
+            float v[4 * C::NV];
+            const float* src = ph + (oy0 + rr) * C::PW + ox0;
+#pragma unroll
+            for (int q = 0; q < C::NV; ++q) {
+                const float4 t = lds128(src + 4 * q);
+                v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+            }
+#pragma unroll
+            for (int a = 0; a < MS; ++a) {
+                const int ro = rr - a;
+                if (ro >= 0 && ro < RB) {
+#pragma unroll
+                    for (int b = 0; b < MS; ++b) {
+                        const float kk = k[a * MS + b];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) force[ro][c] = fmaf(kk, v[c + b], force[ro][c]);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// sum the filter-split partial forces into the split-0 threads (in split
+// order); the others return false.  `red` is free shared memory.
+template <class C, int RB>
+__device__ __forceinline__ bool reduce_splits(float* red, int split, int obx, int oby,
+                                              float (&force)[RB][4]) {
+    if (C::NSPLIT == 1) return true;
+    __syncthreads();  // everyone is done reading sPhi
+    const int slot = (oby * C::OBX + obx) * RB * 4;
+    if (split > 0) {
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                red[(split - 1) * C::OBX * C::OBY * RB * 4 + slot + r * 4 + c] = force[r][c];
+    }
+    __syncthreads();
+    if (split > 0) return false;
+    for (int s2 = 1; s2 < C::NSPLIT; ++s2)
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                force[r][c] += red[(s2 - 1) * C::OBX * C::OBY * RB * 4 + slot + r * 4 + c];
+    return true;
+}
+
+// epilogue of one pixel: u~ = u - force, reaction, checks, store
+__device__ __forceinline__ void finish_pixel(const StageArgs& p, float u, float force,
+                                             const float* __restrict__ fin, float* uout,
+                                             int64_t off, bool& bad, uint32_t& fbits) {
+    float res;
+    if (p.flags & 0x8u) {
+        res = force;
+    } else {
+        const float fv = __ldg(fin + off);
+        if (p.flags & 0x10u) {
+            if (!isfinite(fv)) fbits |= 0x1u;
+            else if (fv < 0.0f) fbits |= 0x2u;
+        }
+        res = reaction(u, force, fv, p);
+    }
+    if (!isfinite(res)) bad = true;
+    uout[off] = res;
+}
+
+__device__ __forceinline__ void report(const StageArgs& p, bool bad, uint32_t fbits) {
+    if (bad) atomicMin(p.status, (uint32_t)p.stage);
+    if (fbits) atomicAnd(p.status + 1, ~fbits);
+}
+
+// ---- tile kernel: one CTA = one output tile, all filter groups -------------
 template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB>
 __global__ void __launch_bounds__(NT, MINB) stage_kernel(const StageArgs p) {
     using C = StageCfg<MS, TH, TW, RF, RB, NT, F>;
@@ -236,39 +497,8 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const StageArgs p) {
     const bool top_halo = p.flags & 0x2u;
     const bool bot_halo = p.flags & 0x4u;
 
-    // prefetch group 0 parameters
-    auto prefetch = [&](int g, int buf) {
-        const float* gt = p.taps + (size_t)g * F * C::KP;
-        float* st = sTap + buf * F * C::KP;
-        for (int i = tid; i < F * C::KP / 4; i += NT) cp_async16(st + 4 * i, gt + 4 * i);
-        const float* gb = p.tab + (size_t)g * tabsz;
-        float* sb = sTab + buf * tabsz;
-        for (int i = tid; i < tabsz / 4; i += NT) cp_async16(sb + 4 * i, gb + 4 * i);
-        cp_async_commit();
-    };
-    prefetch(0, 0);
-
-    // ---- stage u tile (2r halo), mirrored at image edges --------------------
-    {
-        const bool floor_in = p.flags & 0x1u;
-        for (int i = tid; i < C::SU; i += NT) {
-            const int uy = i / C::US, ux = i - uy * C::US;
-            int Y = Y0 - 2 * R + uy;
-            int X = mirror_clamp(X0 - 2 * R + ux, p.W);
-            if (Y < 0) Y = top_halo ? max(Y, -2 * R) : mirror_clamp(Y, p.H);
-            else if (Y >= p.H) Y = bot_halo ? min(Y, p.H - 1 + 2 * R) : mirror_clamp(Y, p.H);
-            float v = __ldg(uin + (int64_t)Y * p.ld + X);
-            if (floor_in) v = fmaxf(v, p.u0_floor);
-            sU[i] = v;
-        }
-    }
-
-    // tile touches a mirrored image edge? (phi halo fix-up needed)
-    const bool fix_l = X0 - R < 0;
-    const bool fix_r = X0 + TW + R > p.W;
-    const bool fix_t = !top_halo && (Y0 - R < 0);
-    const bool fix_b = !bot_halo && (Y0 + TH + R > p.H);
-    const bool need_fix = fix_l || fix_r || fix_t || fix_b;
+    prefetch_group<C, F, NT>(p, sTap, sTab, 0, 0, tid);
+    stage_u_tile<C, NT>(p, sU, uin, Y0, X0, top_halo, bot_halo, tid);
 
     const int split = tid / (C::OBX * C::OBY);            // which filters of a group
     const int obx = tid % C::OBX, oby = (tid / C::OBX) % C::OBY;
@@ -283,188 +513,16 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const StageArgs p) {
         const int buf = g & 1;
         cp_async_wait_all();
         __syncthreads();  // params of group g landed; previous bwd done with sPhi
-        if (g + 1 < p.ngroups) prefetch(g + 1, buf ^ 1);
+        if (g + 1 < p.ngroups) prefetch_group<C, F, NT>(p, sTap, sTab, g + 1, buf ^ 1, tid);
         const float* tapg = sTap + buf * F * C::KP;
         const float* tabg = sTab + buf * tabsz;
-
-        // ---- forward: z = conv(u, k) on the phi region, phi = rbf(z) --------
-        // TPF threads per filter, each with the filter's taps in registers
-        {
-            const int fi = tid / C::TPF;
-            float k[C::KK];
-            {
-                const float4* t4 = reinterpret_cast<const float4*>(tapg + fi * C::KP);
-#pragma unroll
-                for (int q = 0; q < C::KP / 4; ++q) {
-                    const float4 v = t4[q];
-                    if (4 * q + 0 < C::KK) k[4 * q + 0] = v.x;
-                    if (4 * q + 1 < C::KK) k[4 * q + 1] = v.y;
-                    if (4 * q + 2 < C::KK) k[4 * q + 2] = v.z;
-                    if (4 * q + 3 < C::KK) k[4 * q + 3] = v.w;
-                }
-            }
-            const float* tabf = tabg + fi * p.tab_stride;
-            float* phif = sPhi + fi * C::SPHI;
-            for (int blk = tid - fi * C::TPF; blk < C::NBLK; blk += C::TPF) {
-                const int by = blk / C::NBX;
-                const int bx = blk - by * C::NBX;
-                const int x0 = bx * 4, y0 = by * RF;
-                float acc[RF][4];
-#pragma unroll
-                for (int r = 0; r < RF; ++r)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
-#pragma unroll
-                for (int rr = 0; rr < RF + 2 * R; ++rr) {
-                    float v[4 * C::NV];
-                    const float* src = sU + (y0 + rr) * C::US + x0;
-#pragma unroll
-                    for (int q = 0; q < C::NV; ++q) {
-                        const float4 t = lds128(src + 4 * q);
-                        v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
-                    }
-#pragma unroll
-                    for (int a = 0; a < MS; ++a) {
-                        const int ro = rr - a;
-                        if (ro >= 0 && ro < RF) {
-#pragma unroll
-                            for (int b = 0; b < MS; ++b) {
-                                // true convolution == correlation with rot180(k)
-                                const float kk = k[(MS - 1 - a) * MS + (MS - 1 - b)];
-#pragma unroll
-                                for (int c = 0; c < 4; ++c) acc[ro][c] = fmaf(kk, v[c + b], acc[ro][c]);
-                            }
-                        }
-                    }
-                }
-                float* dst = phif + y0 * C::PW + x0;
-#pragma unroll
-                for (int r = 0; r < RF; ++r) {
-                    float4 o;
-                    if (FAST) {
-                        o.x = rbf_poly(acc[r][0], tabf, p);
-                        o.y = rbf_poly(acc[r][1], tabf, p);
-                        o.z = rbf_poly(acc[r][2], tabf, p);
-                        o.w = rbf_poly(acc[r][3], tabf, p);
-                    } else {
-                        o.x = rbf_direct(acc[r][0], tabf, p);
-                        o.y = rbf_direct(acc[r][1], tabf, p);
-                        o.z = rbf_direct(acc[r][2], tabf, p);
-                        o.w = rbf_direct(acc[r][3], tabf, p);
-                    }
-                    *reinterpret_cast<float4*>(dst + r * C::PW) = o;
-                }
-            }
-        }
+        forward_group<C, MS, RF, F, FAST>(p, sU, sPhi, tapg, tabg, tid);
         __syncthreads();
-
-        // ---- phi halo outside the image = mirror of in-image phi -------------
-        if (need_fix) {
-            // only the out-of-image band of the phi region is rewritten: rows
-            // [0, nt) and [h0, C::PH) and, for the rows in between, columns
-            // [0, nl) and [w0, C::PW); sources are in-image (mirror).
-            const int nt_ = fix_t ? min(R, C::PH) : 0;
-            const int h0 = fix_b ? max(nt_, min(C::PH, p.H - (Y0 - R))) : C::PH;
-            const int nl_ = fix_l ? R : 0;
-            const int w0 = fix_r ? max(nl_, min(C::PW, p.W - (X0 - R))) : C::PW;
-            const int full_rows = nt_ + (C::PH - h0);
-            const int mid_rows = h0 - nt_;
-            const int per_f = full_rows * C::PW + mid_rows * (nl_ + C::PW - w0);
-            for (int i = tid; i < F * per_f; i += NT) {
-                const int j = i / per_f;
-                int rem = i - j * per_f;
-                int py, px;
-                if (rem < full_rows * C::PW) {
-                    const int rr = rem / C::PW;
-                    px = rem - rr * C::PW;
-                    py = rr < nt_ ? rr : h0 + (rr - nt_);
-                } else {
-                    rem -= full_rows * C::PW;
-                    const int wcols = nl_ + C::PW - w0;
-                    const int rr = rem / wcols, cc = rem - rr * wcols;
-                    py = nt_ + rr;
-                    px = cc < nl_ ? cc : w0 + (cc - nl_);
-                }
-                const int Y = Y0 - R + py, X = X0 - R + px;
-                int sy = Y, sx = X;
-                if (X < 0 && X >= -R) sx = -1 - X;
-                else if (X >= p.W && X < p.W + R) sx = 2 * p.W - 1 - X;
-                if (!top_halo && Y < 0 && Y >= -R) sy = -1 - Y;
-                else if (!bot_halo && Y >= p.H && Y < p.H + R) sy = 2 * p.H - 1 - Y;
-                if (sy != Y || sx != X) {
-                    const int spy = sy - (Y0 - R), spx = sx - (X0 - R);
-                    sPhi[j * C::SPHI + py * C::PW + px] = sPhi[j * C::SPHI + spy * C::PW + spx];
-                }
-            }
-            __syncthreads();
-        }
-
-        // ---- backward: force += corr(phi_i, k_i) -----------------------------
-#pragma unroll 1
-        for (int fi = split; fi < F; fi += C::NSPLIT) {
-            float k[C::KK];
-            {
-                const float4* t4 = reinterpret_cast<const float4*>(tapg + fi * C::KP);
-#pragma unroll
-                for (int q = 0; q < C::KP / 4; ++q) {
-                    const float4 v = t4[q];
-                    if (4 * q + 0 < C::KK) k[4 * q + 0] = v.x;
-                    if (4 * q + 1 < C::KK) k[4 * q + 1] = v.y;
-                    if (4 * q + 2 < C::KK) k[4 * q + 2] = v.z;
-                    if (4 * q + 3 < C::KK) k[4 * q + 3] = v.w;
-                }
-            }
-            const float* ph = sPhi + fi * C::SPHI;
-#pragma unroll
-            for (int rr = 0; rr < RB + 2 * R; ++rr) {
-                float v[4 * C::NV];
-                const float* src = ph + (oy0 + rr) * C::PW + ox0;
-#pragma unroll
-                for (int q = 0; q < C::NV; ++q) {
-                    const float4 t = lds128(src + 4 * q);
-                    v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
-                }
-#pragma unroll
-                for (int a = 0; a < MS; ++a) {
-                    const int ro = rr - a;
-                    if (ro >= 0 && ro < RB) {
-#pragma unroll
-                        for (int b = 0; b < MS; ++b) {
-                            const float kk = k[a * MS + b];
-#pragma unroll
-                            for (int c = 0; c < 4; ++c) force[ro][c] = fmaf(kk, v[c + b], force[ro][c]);
-                        }
-                    }
-                }
-            }
-        }
+        fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
+        backward_group<C, MS, RB, F>(sPhi, tapg, split, ox0, oy0, force);
     }
+    if (!reduce_splits<C, RB>(sPhi, split, obx, oby, force)) return;
 
-    // ---- sum the filter-split partial forces --------------------------------
-    if (C::NSPLIT > 1) {
-        __syncthreads();  // everyone is done reading sPhi
-        float* red = sPhi;
-        const int slot = (oby * C::OBX + obx) * RB * 4;
-        if (split > 0) {
-#pragma unroll
-            for (int r = 0; r < RB; ++r)
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    red[(split - 1) * C::OBX * C::OBY * RB * 4 + slot + r * 4 + c] = force[r][c];
-        }
-        __syncthreads();
-        if (split > 0) return;
-        for (int s2 = 1; s2 < C::NSPLIT; ++s2)
-#pragma unroll
-            for (int r = 0; r < RB; ++r)
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    force[r][c] += red[(s2 - 1) * C::OBX * C::OBY * RB * 4 + slot + r * 4 + c];
-    }
-
-    // ---- epilogue: u~ = u - force, prox, checks, store ----------------------
-    const bool out_force = p.flags & 0x8u;
-    const bool check_f = p.flags & 0x10u;
     bool bad = false;
     uint32_t fbits = 0;
 #pragma unroll
@@ -475,24 +533,166 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const StageArgs p) {
         for (int c = 0; c < 4; ++c) {
             const int X = X0 + ox0 + c;
             if (X >= p.W) continue;
-            float res;
-            if (out_force) {
-                res = force[r][c];
-            } else {
-                const float u = sU[(oy0 + r + 2 * R) * C::US + ox0 + c + 2 * R];
-                const float fv = __ldg(fin + (int64_t)Y * p.ld + X);
-                if (check_f) {
-                    if (!isfinite(fv)) fbits |= 0x1u;
-                    else if (fv < 0.0f) fbits |= 0x2u;
-                }
-                res = reaction(u, force[r][c], fv, p);
-            }
-            if (!isfinite(res)) bad = true;
-            uout[(int64_t)Y * p.ld + X] = res;
+            finish_pixel(p, sU[(oy0 + r + 2 * R) * C::US + ox0 + c + 2 * R], force[r][c], fin, uout,
+                         (int64_t)Y * p.ld + X, bad, fbits);
         }
     }
-    if (bad) atomicMin(p.status, (uint32_t)p.stage);
-    if (fbits) atomicAnd(p.status + 1, ~fbits);
+    report(p, bad, fbits);
+}
+
+// ---- split kernels: work units = (tile, filter group) ----------------------
+//
+// For grids too small to fill 148 SMs with whole tiles (a single 512^2 image
+// has 64 large / 256 small tiles) a stage runs as two launches:
+//
+//   stage_kernel_split  a persistent grid of (SMs x resident CTAs) computes
+//       (tile, filter group) units: one group's partial force over one tile,
+//       stored to the workspace.  CTA c takes the c-th of gridDim.x
+//       contiguous, balanced ranges of the tile-major unit sequence (the u
+//       tile is staged once per tile the range touches).
+//   stage_reduce_kernel  sums each pixel's ngroups partials IN GROUP ORDER
+//       and runs the epilogue, over all SMs.
+//
+// The summation order is fixed by the unit structure, not by which CTA ran
+// what, so results are bit-reproducible and identical for any grid (strips
+// == whole image).  No state survives a launch.
+struct SplitWs {
+    float* part;       // [tiles][ngroups][TH*TW] partial forces
+    int tiles_x, tiles_y, tiles;
+};
+
+#ifdef TNRD_SPLIT_TRACE
+// per-CTA timeline for tools/split_trace.py: smid, t0, t1, units | first << 32
+__device__ unsigned long long g_split_trace[4096][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB>
+__global__ void __launch_bounds__(NT, MINB) stage_kernel_split(const StageArgs p, const SplitWs ws) {
+#ifdef TNRD_SPLIT_TRACE
+    const unsigned long long tr_t0 = gtimer();
+#endif
+    using C = StageCfg<MS, TH, TW, RF, RB, NT, F>;
+    constexpr int TPX = TH * TW;
+    extern __shared__ __align__(16) float smem[];
+    float* sU = smem;
+    float* sPhi = sU + C::SU;
+    float* sTap = sPhi + F * C::SPHI;
+    float* sTab = sTap + 2 * F * C::KP;
+    const int tabsz = F * p.tab_stride;
+    const int tid = threadIdx.x;
+    const int ng = p.ngroups;
+    const bool top_halo = p.flags & 0x2u;
+    const bool bot_halo = p.flags & 0x4u;
+
+    const int units = ws.tiles * ng;
+    const int nb = units / (int)gridDim.x, extra = units % (int)gridDim.x;
+    const int c = blockIdx.x;
+    const int ubeg = c * nb + min(c, extra);
+    const int uend = ubeg + nb + (c < extra ? 1 : 0);
+
+    const int split = tid / (C::OBX * C::OBY);
+    const int obx = tid % C::OBX, oby = (tid / C::OBX) % C::OBY;
+    const int ox0 = obx * 4, oy0 = oby * RB;
+
+    if (ubeg < uend) prefetch_group<C, F, NT>(p, sTap, sTab, ubeg % ng, 0, tid);
+    int buf = 0, cur_tile = -1;
+    for (int unit = ubeg; unit < uend; ++unit) {
+        const int tile = unit / ng, g = unit - tile * ng;
+        const int img = tile / (ws.tiles_x * ws.tiles_y);
+        const int trem = tile - img * (ws.tiles_x * ws.tiles_y);
+        const int Y0 = (trem / ws.tiles_x) * TH, X0 = (trem % ws.tiles_x) * TW;
+        if (tile != cur_tile) {
+            __syncthreads();  // the previous unit is done with sU
+            stage_u_tile<C, NT>(p, sU, p.u_in + (int64_t)img * p.img_stride, Y0, X0, top_halo,
+                                bot_halo, tid);
+            cur_tile = tile;
+        }
+        cp_async_wait_all();
+        __syncthreads();  // params + u tile in smem; previous unit done with sPhi
+        if (unit + 1 < uend) prefetch_group<C, F, NT>(p, sTap, sTab, (unit + 1) % ng, buf ^ 1, tid);
+        const float* tapg = sTap + buf * F * C::KP;
+        const float* tabg = sTab + buf * tabsz;
+        forward_group<C, MS, RF, F, FAST>(p, sU, sPhi, tapg, tabg, tid);
+        __syncthreads();
+        fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
+        float force[RB][4];
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) force[r][cc] = 0.0f;
+        backward_group<C, MS, RB, F>(sPhi, tapg, split, ox0, oy0, force);
+        if (reduce_splits<C, RB>(sPhi, split, obx, oby, force)) {
+            float* dst = ws.part + ((size_t)tile * ng + g) * TPX + oy0 * TW + ox0;
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+                __stcg(reinterpret_cast<float4*>(dst + r * TW),
+                       make_float4(force[r][0], force[r][1], force[r][2], force[r][3]));
+        }
+        buf ^= 1;
+    }
+#ifdef TNRD_SPLIT_TRACE
+    if (tid == 0 && blockIdx.x < 4096) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_split_trace[blockIdx.x][0] = smid;
+        g_split_trace[blockIdx.x][1] = tr_t0;
+        g_split_trace[blockIdx.x][2] = gtimer();
+        g_split_trace[blockIdx.x][3] = (unsigned long long)(uend - ubeg) | ((unsigned long long)(unsigned)ubeg << 32);
+    }
+#endif
+}
+
+// sum of a pixel quad's partials in group order, then the epilogue (u from
+// u_in, floored on the first stage exactly as the tile kernels stage it)
+template <int TH, int TW>
+__global__ void __launch_bounds__(128) stage_reduce_kernel(const StageArgs p, const SplitWs ws) {
+    constexpr int TPX = TH * TW;
+    const int ng = p.ngroups;
+    const int64_t quads = (int64_t)ws.tiles * (TPX / 4);
+    bool bad = false;
+    uint32_t fbits = 0;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < quads;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int tile = (int)(q / (TPX / 4));
+        const int i = 4 * (int)(q - (int64_t)tile * (TPX / 4));
+        const int img = tile / (ws.tiles_x * ws.tiles_y);
+        const int trem = tile - img * (ws.tiles_x * ws.tiles_y);
+        const int Y = (trem / ws.tiles_x) * TH + i / TW;
+        const int Xq = (trem % ws.tiles_x) * TW + i % TW;
+        if (Y >= p.H) continue;
+        const float* src = ws.part + (size_t)tile * ng * TPX + i;
+        float4 acc = __ldcg(reinterpret_cast<const float4*>(src));
+        for (int g0 = 1; g0 < ng; g0 += 8) {
+            float4 v[8];  // 8 loads in flight, then the adds in group order
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (g0 + k < ng) v[k] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)(g0 + k) * TPX));
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (g0 + k < ng) {
+                    acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w;
+                }
+        }
+        const float fa[4] = {acc.x, acc.y, acc.z, acc.w};
+        const float* __restrict__ uin = p.u_in + (int64_t)img * p.img_stride;
+        const float* __restrict__ fin = p.f + (int64_t)img * p.img_stride;
+        float* __restrict__ uout = p.u_out + (int64_t)img * p.img_stride;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int X = Xq + c;
+            if (X >= p.W) continue;
+            const int64_t off = (int64_t)Y * p.ld + X;
+            float u = __ldg(uin + off);
+            if (p.flags & 0x1u) u = fmaxf(u, p.u0_floor);
+            finish_pixel(p, u, fa[c], fin, uout, off, bad, fbits);
+        }
+    }
+    report(p, bad, fbits);
 }
 
 }  // namespace tnrd

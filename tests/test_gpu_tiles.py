@@ -1,6 +1,8 @@
-"""Both CUDA-core tile configurations (32x32 / 4-filter groups and
-64x64 / 2-filter groups; bench workloads pick one by grid size) meet the
-parity bar and agree bit-for-bit on their strip-mode and batch semantics."""
+"""Every CUDA-core stage configuration -- the tile kernel with 32x32 /
+4-filter groups and 64x64 / 2-filter groups, and the split kernel ((tile,
+group) units + ordered reduction) with either tile -- meets the parity bar
+and agrees bit-for-bit on its strip-mode and batch semantics (auto picks one
+by grid size)."""
 import numpy as np
 import pytest
 
@@ -12,7 +14,9 @@ from paper_1702_07482_b200 import _lib, synth
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=[_lib.KERNEL_SMALL_TILES, _lib.KERNEL_LARGE_TILES], ids=["small", "large"])
+@pytest.fixture(params=[_lib.KERNEL_SMALL_TILES, _lib.KERNEL_LARGE_TILES,
+                        _lib.KERNEL_SPLIT_LARGE, _lib.KERNEL_SPLIT_SMALL],
+                ids=["small", "large", "split_large", "split_small"])
 def tiles(cuda, request):
     _lib.set_stage_kernel(request.param)
     yield request.param
@@ -70,4 +74,48 @@ def test_auto_large_tiles_batch_matches_small(cuda):
         b = tn.run_diffusion_batch(f, model).cpu().numpy()
     finally:
         _lib.set_stage_kernel(_lib.KERNEL_AUTO)
+    assert np.max(np.abs(a - b) / b) < 1e-5
+
+
+@pytest.mark.parametrize("mode", [_lib.KERNEL_SPLIT_LARGE, _lib.KERNEL_SPLIT_SMALL])
+def test_split_kernel_reproducible_and_shape_independent(cuda, mode):
+    """The split kernel's ordered reduction makes a pixel's value independent
+    of which CTA ran which unit: repeated runs, a batch vs its images one by
+    one, and the same image after other shapes reused the workspace are all
+    bit-identical."""
+    torch = cuda
+    model = synth.make_model(7, 12, 3, 63, seed=11)
+    dm = tn.device_model_for(model)
+    rng = np.random.default_rng(4)
+    fs = [rng.uniform(0, 300, (150, 170)).astype(np.float32) for _ in range(3)]
+    _lib.set_stage_kernel(mode)
+    try:
+        fb = torch.from_numpy(np.stack(fs)).cuda()
+        ub = dm.despeckle(fb)
+        assert torch.equal(ub, dm.despeckle(fb))
+        dm.despeckle(torch.from_numpy(rng.uniform(0, 300, (300, 40)).astype(np.float32)).cuda())
+        for i, fi in enumerate(fs):
+            assert torch.equal(dm.despeckle(torch.from_numpy(fi).cuda()), ub[i])
+    finally:
+        _lib.set_stage_kernel(_lib.KERNEL_AUTO)
+
+
+def test_auto_small_grid_uses_split_and_matches_tile_kernel(cuda):
+    """A single C2 image (auto: split kernel) agrees with the whole-tile
+    kernel to fp32 summation order and runs 2 launches per stage."""
+    torch = cuda
+    cfg = synth.CONFIGS["c2"]
+    model = synth.config_model(cfg)
+    f = torch.from_numpy(synth.noisy_image(cfg, 0)[1]).cuda()
+    dm = tn.device_model_for(model)
+    _lib.launch_count_reset()
+    a = dm.despeckle(f)
+    torch.cuda.synchronize()
+    assert _lib.launch_count() == 2 * cfg.T
+    _lib.set_stage_kernel(_lib.KERNEL_LARGE_TILES)
+    try:
+        b = dm.despeckle(f)
+    finally:
+        _lib.set_stage_kernel(_lib.KERNEL_AUTO)
+    a, b = a.cpu().numpy(), b.cpu().numpy()
     assert np.max(np.abs(a - b) / b) < 1e-5
