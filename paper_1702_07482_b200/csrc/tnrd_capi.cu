@@ -89,9 +89,9 @@ struct tnrd_model {
     // [nk_pad/16 groups][m][ksteps][2 prec][2 kc][16][4]
     float* d_bop = nullptr;
     size_t bop_stage = 0;     // floats per stage
-    // split-kernel workspaces, one per stream (launches on one stream are
-    // ordered, so a stream's workspace is never used by two kernels at once);
-    // zero-filled at allocation and left zeroed by every split launch
+    // split-kernel partial-force workspaces, one per stream (launches on one
+    // stream are ordered, so a stream's workspace is never used by two
+    // kernels at once); nothing in them outlives a stage
     struct SplitBuf { void* ptr = nullptr; size_t bytes = 0; };
     mutable std::mutex ws_mu;
     mutable std::map<cudaStream_t, SplitBuf> ws;
@@ -410,6 +410,27 @@ struct SplitTile { static constexpr int TH = 64, TW = 64, RF = TNRD_LARGE_RF, RB
 
 constexpr size_t kMaxSplitBytes = size_t(1) << 30;
 
+// Launch with programmatic stream serialization: the kernel may be scheduled
+// while its predecessor on the stream drains, and waits for it with
+// griddepcontrol.wait before touching the predecessor's output (the split
+// kernel's unit / reduction pair, and consecutive stages, overlap their
+// launch latency this way).
+template <class... KArgs, class... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, int block, size_t smem,
+                              cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int MS, bool FAST, class T>
 struct StageKernel {
     static constexpr int TH = T::TH, TW = T::TW, RB = T::RB, NT = T::NT, F = T::F;
@@ -439,11 +460,9 @@ struct StageKernel {
         auto kern = stage_kernel<MS, TH, TW, RF, RB, NT, FAST, F, MINB>;
         int rc = prepare(kern, dev, attr_set, mu);
         if (rc) return rc;
-        dim3 grid((a.W + TW - 1) / TW, (a.H + TH - 1) / TH, batch);
         StageArgs b = a;
         b.ngroups = (a.nk + F - 1) / F;
-        kern<<<grid, NT, smem, s>>>(b);
-        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(launch_pdl(kern, dim3((a.W + TW - 1) / TW, (a.H + TH - 1) / TH, batch), NT, smem, s, b));
         g_launches.fetch_add(1);
         return TNRD_OK;
     }
@@ -486,12 +505,10 @@ struct StageKernel {
         w.part = static_cast<float*>(wsp);
         const long units = (long)w.tiles * b.ngroups;
         const int grid = (int)std::min<long>(units, (long)sms * per_sm);
-        kern<<<grid, NT, smem, s>>>(b, w);
-        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(launch_pdl(kern, grid, NT, smem, s, b, w));
         const long quads = (long)w.tiles * (TH * TW / 4);
         const int rgrid = (int)std::min<long>((quads + 127) / 128, (long)sms * 16);
-        stage_reduce_kernel<TH, TW><<<rgrid, 128, 0, s>>>(b, w);
-        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(launch_pdl(stage_reduce_kernel<TH, TW>, rgrid, 128, 0, s, b, w));
         g_launches.fetch_add(2);
         return TNRD_OK;
     }
@@ -567,7 +584,7 @@ static int dispatch_split_m_t(int m, const StageArgs& a, int batch, void* ws, cu
     }
 }
 
-// the stream's split workspace, grown (zero-filled) on demand
+// the stream's split workspace, grown on demand (outside stream capture)
 static int split_workspace(const tnrd_model* md, cudaStream_t s, size_t bytes, void** out) {
     std::lock_guard<std::mutex> lk(md->ws_mu);
     auto& b = md->ws[s];
@@ -583,7 +600,6 @@ static int split_workspace(const tnrd_model* md, cudaStream_t s, size_t bytes, v
             b.bytes = 0;
         }
         CUDA_TRY(cudaMalloc(&b.ptr, bytes));
-        CUDA_TRY(cudaMemset(b.ptr, 0, bytes));
         b.bytes = bytes;
     }
     *out = b.ptr;

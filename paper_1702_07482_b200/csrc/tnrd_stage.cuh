@@ -470,6 +470,28 @@ __device__ __forceinline__ void finish_pixel(const StageArgs& p, float u, float 
     uout[off] = res;
 }
 
+// finish_pixel with the observation already loaded
+__device__ __forceinline__ void finish_pixel_f(const StageArgs& p, float u, float force, float fv,
+                                               float* uout, int64_t off, bool& bad, uint32_t& fbits) {
+    float res;
+    if (p.flags & 0x8u) {
+        res = force;
+    } else {
+        if (p.flags & 0x10u) {
+            if (!isfinite(fv)) fbits |= 0x1u;
+            else if (fv < 0.0f) fbits |= 0x2u;
+        }
+        res = reaction(u, force, fv, p);
+    }
+    if (!isfinite(res)) bad = true;
+    uout[off] = res;
+}
+
+// programmatic dependent launch: wait for the predecessor grid's completion
+// (and memory) / let the successor grid be scheduled
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void report(const StageArgs& p, bool bad, uint32_t fbits) {
     if (bad) atomicMin(p.status, (uint32_t)p.stage);
     if (fbits) atomicAnd(p.status + 1, ~fbits);
@@ -498,6 +520,8 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const StageArgs p) {
     const bool bot_halo = p.flags & 0x4u;
 
     prefetch_group<C, F, NT>(p, sTap, sTab, 0, 0, tid);
+    pdl_wait();     // the previous stage wrote u_in
+    pdl_trigger();
     stage_u_tile<C, NT>(p, sU, uin, Y0, X0, top_halo, bot_halo, tid);
 
     const int split = tid / (C::OBX * C::OBY);            // which filters of a group
@@ -600,6 +624,8 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel_split(const StageArgs p
     const int ox0 = obx * 4, oy0 = oby * RB;
 
     if (ubeg < uend) prefetch_group<C, F, NT>(p, sTap, sTab, ubeg % ng, 0, tid);
+    pdl_wait();     // the previous stage wrote u_in
+    pdl_trigger();  // the reduction may be scheduled as CTAs retire
     int buf = 0, cur_tile = -1;
     for (int unit = ubeg; unit < uend; ++unit) {
         const int tile = unit / ng, g = unit - tile * ng;
@@ -648,14 +674,19 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel_split(const StageArgs p
 }
 
 // sum of a pixel quad's partials in group order, then the epilogue (u from
-// u_in, floored on the first stage exactly as the tile kernels stage it)
+// u_in, floored on the first stage exactly as the tile kernels stage it).
+// Up to 24 groups all partial loads of a quad are in flight at once, with
+// the quad's u and f loads.
 template <int TH, int TW>
 __global__ void __launch_bounds__(128) stage_reduce_kernel(const StageArgs p, const SplitWs ws) {
     constexpr int TPX = TH * TW;
+    constexpr int NV = 24;
     const int ng = p.ngroups;
     const int64_t quads = (int64_t)ws.tiles * (TPX / 4);
     bool bad = false;
     uint32_t fbits = 0;
+    pdl_wait();     // all partials written
+    pdl_trigger();
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < quads;
          q += (int64_t)gridDim.x * blockDim.x) {
         const int tile = (int)(q / (TPX / 4));
@@ -665,31 +696,39 @@ __global__ void __launch_bounds__(128) stage_reduce_kernel(const StageArgs p, co
         const int Y = (trem / ws.tiles_x) * TH + i / TW;
         const int Xq = (trem % ws.tiles_x) * TW + i % TW;
         if (Y >= p.H) continue;
-        const float* src = ws.part + (size_t)tile * ng * TPX + i;
-        float4 acc = __ldcg(reinterpret_cast<const float4*>(src));
-        for (int g0 = 1; g0 < ng; g0 += 8) {
-            float4 v[8];  // 8 loads in flight, then the adds in group order
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if (g0 + k < ng) v[k] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)(g0 + k) * TPX));
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if (g0 + k < ng) {
-                    acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w;
-                }
-        }
-        const float fa[4] = {acc.x, acc.y, acc.z, acc.w};
         const float* __restrict__ uin = p.u_in + (int64_t)img * p.img_stride;
         const float* __restrict__ fin = p.f + (int64_t)img * p.img_stride;
         float* __restrict__ uout = p.u_out + (int64_t)img * p.img_stride;
+        float uq[4], fq[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int64_t off = (int64_t)Y * p.ld + min(Xq + c, p.W - 1);
+            uq[c] = __ldg(uin + off);
+            fq[c] = __ldg(fin + off);
+        }
+        const float* src = ws.part + (size_t)tile * ng * TPX + i;
+        float4 v[NV];
+#pragma unroll
+        for (int g = 0; g < NV; ++g)
+            if (g < ng) v[g] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)g * TPX));
+        float4 acc = v[0];
+#pragma unroll
+        for (int g = 1; g < NV; ++g)
+            if (g < ng) {
+                acc.x += v[g].x; acc.y += v[g].y; acc.z += v[g].z; acc.w += v[g].w;
+            }
+        for (int g = NV; g < ng; ++g) {
+            const float4 w = __ldcg(reinterpret_cast<const float4*>(src + (size_t)g * TPX));
+            acc.x += w.x; acc.y += w.y; acc.z += w.z; acc.w += w.w;
+        }
+        const float fa[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const int X = Xq + c;
             if (X >= p.W) continue;
-            const int64_t off = (int64_t)Y * p.ld + X;
-            float u = __ldg(uin + off);
+            float u = uq[c];
             if (p.flags & 0x1u) u = fmaxf(u, p.u0_floor);
-            finish_pixel(p, u, fa[c], fin, uout, off, bad, fbits);
+            finish_pixel_f(p, u, fa[c], fq[c], uout, (int64_t)Y * p.ld + X, bad, fbits);
         }
     }
     report(p, bad, fbits);
