@@ -421,7 +421,11 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the fused stage kernel (SURVEY 8(d) algorithmic work)
+    # ---- roofline of the fused stage (SURVEY 8(d) algorithmic work); small
+    # grids run it as the split kernel + its ordered reduction (2 launches)
+    stage_kernels = int(round(launches / (args.steps * cfg.T)))
+    stage_kernels = {1: "stage_kernel (fused tile kernel)",
+                     2: "stage_kernel_split + stage_reduce_kernel"}.get(stage_kernels, str(stage_kernels))
     px_launch = px_rank
     flop_launch = w_flop(cfg) * px_launch
     achieved_tf = flop_launch / (launch_ms * 1e-3) / 1e12
@@ -449,8 +453,9 @@ def main():
             "bound": "fp32", "unit": "TFLOP/s", "achieved": achieved_tf,
             "peak": peak_tf, "frac": achieved_tf / peak_tf, "traffic": traffic,
             "peak_source": "measured on this GPU by tnrd_probe (FFMA); MEASURED_PEAKS.json has no FP32/MUFU entry",
-            "work": f"SURVEY 8(d): W_flop={w_flop(cfg)} FLOP/pixel-stage x {px_launch} px per launch",
+            "work": f"SURVEY 8(d): W_flop={w_flop(cfg)} FLOP/pixel-stage x {px_launch} px per stage",
             "launch_ms": launch_ms,
+            "stage_kernels": stage_kernels,
             "survey_combined": {
                 "unit": "MPix*stages/s", "achieved": ach_pxst, "peak": roof_pxst,
                 "frac": ach_pxst / roof_pxst,

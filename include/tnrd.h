@@ -99,10 +99,15 @@ int tnrd_model_rbf_fit(const tnrd_model* model, double* max_abs_err,
                        int* intervals);
 
 /* Stage kernel selection (process-wide): 0 = auto (the kernel measured
- * fastest on B200), 1 = CUDA-core kernel, 2 = tcgen05
- * forward-GEMM kernel (error if the model is unsupported: m > 7 or RBF
- * tables too large), 3 / 4 = CUDA-core kernel with its small (32x32) /
- * large (64x64) tile configuration forced. */
+ * fastest on B200 for the grid size), 1 = CUDA-core kernels
+ * (same choice as auto), 2 = tcgen05 forward-GEMM kernel (error if the
+ * model is unsupported: m > 7 or RBF tables too large), 3 / 4 = CUDA-core
+ * tile kernel with its small (32x32) / large (64x64) tiles forced, 5 = the
+ * phase-locked tcgen05 kernel, 6 / 7 = CUDA-core split kernel ((tile,
+ * filter group) units + ordered reduction, 2 launches per stage) with
+ * large / small tiles forced.  Auto runs the split kernel on grids below
+ * 3 waves of large tiles; it keeps a partial-force workspace per stream
+ * inside the model (allocated on first use, outside stream capture). */
 int tnrd_set_stage_kernel(int mode);
 
 /* Reset a device status block (stream-ordered memset). */
