@@ -18,6 +18,8 @@
  *                            reference's only calling convention)
  *   tnrd_conv2d           <- conv2d                   (imageops.py:53-72)
  *   tnrd_prox_idiv        <- prox_idiv                (speckle.py:111-121)
+ *   tnrd_sample_speckle   <- sample_speckle/speckle_field (speckle.py:51-70),
+ *                            statistical parity (own counter-based generator)
  *
  * Conventions
  *   - images are fp32, row-major, `ld` elements between rows and
@@ -154,6 +156,23 @@ float* tnrd_plan_u_device(tnrd_plan* plan);
 
 /* Same-size true convolution with half-sample mirror padding (conv2d,
  * imageops.py:53-72); k: m*m float64 host array, m odd, m <= 15. */
+/* L-look amplitude speckle on the GPU (speckle.py:51-70, SURVEY §8(f) rank
+ * 3): out = clean * sqrt(G / L), G ~ Gamma(L, 1) per pixel; clean == NULL
+ * writes the field sqrt(G / L) itself.  Generator: Philox4x32-10 keyed by
+ * `seed`, counter (pixel index, attempt, 0) with pixel index = image*H*W +
+ * y*W + x, and Marsaglia-Tsang gamma (tnrd_speckle.cuh).  Bit-reproducible
+ * for a given (seed, looks, shape) under any launch geometry; equal to the
+ * reference's numpy Generator(Philox).gamma in distribution only (the
+ * reference's sequential rejection stream has no parallel equivalent).
+ * With d_status (may be NULL) a non-finite / negative clean pixel clears
+ * bit 0 / 1 of d_status[1] (decoded by tnrd_status_decode as bad input). */
+int tnrd_sample_speckle(const float* clean, float* out, int batch, int H,
+                        int W, int64_t ld, int64_t image_stride, int looks,
+                        uint64_t seed, uint32_t* d_status, void* stream);
+/* The generator's integer core on the host (known-answer tests). */
+void tnrd_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2],
+                        uint32_t out[4]);
+
 int tnrd_conv2d(const float* img, float* out, int H, int W, int64_t ld,
                 const double* k, int m, void* stream);
 /* Closed-form I-divergence prox (prox_idiv, speckle.py:111-121). */

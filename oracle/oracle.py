@@ -76,6 +76,12 @@ def lib():
         L.oracle_max_threads.restype = ctypes.c_int
         L.oracle_set_threads.restype = None
         L.oracle_set_threads.argtypes = [ctypes.c_int]
+        _u32p = ctypes.POINTER(ctypes.c_uint32)
+        L.oracle_philox4x32_10.argtypes = [_u32p, _u32p, _u32p]
+        L.oracle_philox4x32_10.restype = None
+        L.oracle_speckle_field.argtypes = [_dp, ctypes.c_long, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_uint64, ctypes.c_uint64]
+        L.oracle_speckle_field.restype = None
         L.oracle_set_threads(-1)  # default: every host core
         _lib = L
     return _lib
@@ -234,3 +240,21 @@ def psnr(test, reference, peak: float) -> float:
 
 def threads() -> int:
     return int(lib().oracle_max_threads())
+
+
+def philox4x32_10(ctr, key) -> tuple:
+    """Philox4x32-10 block (the GPU speckle generator's integer core)."""
+    c = (ctypes.c_uint32 * 4)(*ctr)
+    k = (ctypes.c_uint32 * 2)(*key)
+    o = (ctypes.c_uint32 * 4)()
+    lib().oracle_philox4x32_10(c, k, o)
+    return tuple(o)
+
+
+def speckle_field(shape, looks: int, seed: int, base: int = 0) -> np.ndarray:
+    """float64 restatement of tnrd_sample_speckle's field sqrt(G/L) for the
+    pixel indices base .. base + prod(shape) (see tnrd_oracle.c)."""
+    out = np.empty(int(np.prod(shape)), dtype=np.float64)
+    lib().oracle_speckle_field(_p(out), out.size, int(shape[-1]), int(looks), int(seed),
+                               int(base))
+    return out.reshape(shape)

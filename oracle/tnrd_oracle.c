@@ -24,9 +24,17 @@
  *                        u_next = prox(u~, f, lam).
  *   oracle_run_diffusion diffusion.py:219-242 u0 = max(f, 1e-6); T stages;
  *                        non-finite check after every stage.
+ *   oracle_speckle_field speckle.py:51-61 amplitude speckle sqrt(G/L),
+ *                        G ~ Gamma(L, 1), restated with the GPU path's
+ *                        generator (Philox4x32-10, counter = pixel index /
+ *                        block, Marsaglia-Tsang) in float64: the checker for
+ *                        tnrd_sample_speckle.  The reference's numpy stream
+ *                        (Generator(Philox).gamma) is matched in distribution
+ *                        by the tests, not bitwise (no parallel equivalent).
  */
 #include <math.h>
 #include <pthread.h>
+#include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 #include <unistd.h>
@@ -242,3 +250,73 @@ int oracle_run_diffusion_ex(const double* f, int H, int W, int m, int nk, int T,
 }
 
 int oracle_max_threads(void) { return g_threads; }
+
+/* ---- speckle (see header) ------------------------------------------------ */
+
+typedef struct { uint32_t v[4]; } ph4;
+
+static ph4 philox10(ph4 c, uint32_t k0, uint32_t k1) {
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c.v[0];
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.v[2];
+        ph4 n;
+        n.v[0] = (uint32_t)(p1 >> 32) ^ c.v[1] ^ k0;
+        n.v[1] = (uint32_t)p1;
+        n.v[2] = (uint32_t)(p0 >> 32) ^ c.v[3] ^ k1;
+        n.v[3] = (uint32_t)p0;
+        c = n;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    ph4 c = {{ctr[0], ctr[1], ctr[2], ctr[3]}};
+    c = philox10(c, key[0], key[1]);
+    for (int i = 0; i < 4; ++i) out[i] = c.v[i];
+}
+
+static double u01d(uint32_t b) { return ((double)(b >> 8) + 0.5) / 16777216.0; }
+
+static int mt_try_d(double d, double c, double x, double u, double* g) {
+    const double t = 1.0 + c * x;
+    if (t <= 0.0) return 0;
+    const double v = t * t * t;
+    if (log(u) < 0.5 * x * x + d - d * v + d * log(v)) { *g = d * v; return 1; }
+    return 0;
+}
+
+static void box_muller_d(uint32_t b1, uint32_t b2, double* n0, double* n1) {
+    const double rad = sqrt(-2.0 * log(u01d(b1)));
+    const double th = 2.0 * M_PI * u01d(b2) - M_PI;
+    *n0 = -rad * cos(th);
+    *n1 = -rad * sin(th);
+}
+
+/* sqrt(Gamma(L,1)/L) of the pixel at flat index idx (tnrd_speckle.cuh) */
+static double speckle_px(uint64_t idx, int looks, uint32_t k0, uint32_t k1) {
+    const double d = looks - 1.0 / 3.0, c = 1.0 / sqrt(9.0 * d);
+    for (uint32_t att = 0;; ++att) {
+        ph4 in = {{(uint32_t)idx, (uint32_t)(idx >> 32), att, 0u}};
+        const ph4 r = philox10(in, k0, k1);
+        double n0, n1, g;
+        box_muller_d(r.v[0], r.v[1], &n0, &n1);
+        if (mt_try_d(d, c, n0, u01d(r.v[2]), &g)) return sqrt(g / looks);
+        if (mt_try_d(d, c, n1, u01d(r.v[3]), &g)) return sqrt(g / looks);
+    }
+}
+
+typedef struct { double* out; int looks, W; uint32_t k0, k1; uint64_t base; } sp_ctx;
+
+static void speckle_range(long lo, long hi, void* vctx) {
+    sp_ctx* c = (sp_ctx*)vctx;
+    for (long i = lo; i < hi; ++i)
+        c->out[i] = speckle_px(c->base + (uint64_t)i, c->looks, c->k0, c->k1);
+}
+
+/* field values of flat pixel indices [base, base + n), rows of width W */
+void oracle_speckle_field(double* out, long n, int W, int looks, uint64_t seed, uint64_t base) {
+    sp_ctx c = {out, looks, W, (uint32_t)seed, (uint32_t)(seed >> 32), base};
+    par_for(n, speckle_range, &c);
+}

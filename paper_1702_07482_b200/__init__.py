@@ -14,7 +14,9 @@ from .engine import DeviceModel, device_model_for
 from .imageops import as_image, as_kernel, conv2d, rotate180
 from .influence import RbfGrid
 from .speckle import (F_FLOOR, NoisyPair, SpeckleConfig, prox_idiv,
-                      sample_speckle, speckle_field)
+                      nakagami_mean, sample_speckle, sample_speckle_device,
+                      sample_speckle_gpu,
+                      speckle_field, speckle_field_device)
 
 __all__ = [
     "VARIANTS", "DiffusionModel", "StageParams", "StageTrace",
@@ -24,7 +26,8 @@ __all__ = [
     "DeviceModel",
     "device_model_for", "as_image", "as_kernel", "conv2d", "rotate180",
     "RbfGrid", "F_FLOOR", "NoisyPair", "SpeckleConfig", "prox_idiv",
-    "sample_speckle", "speckle_field",
+    "sample_speckle", "speckle_field", "sample_speckle_device",
+    "sample_speckle_gpu", "speckle_field_device", "nakagami_mean",
 ]
 
 __version__ = "0.1.0"

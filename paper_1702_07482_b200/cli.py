@@ -16,7 +16,7 @@ import sys
 
 from . import io as tio
 from .diffusion import run_diffusion
-from .speckle import SpeckleConfig, sample_speckle
+from .speckle import SpeckleConfig, sample_speckle, sample_speckle_gpu
 
 log = logging.getLogger("paper_1702_07482_b200")
 
@@ -39,6 +39,9 @@ def build_parser() -> argparse.ArgumentParser:
     si.add_argument("--looks", type=int, default=1)
     si.add_argument("--seed", type=int, default=0)
     si.add_argument("--peak", type=float, default=255.0)
+    si.add_argument("--gpu", action="store_true",
+                    help="draw the speckle on the GPU (same distribution, not the "
+                         "reference's bit stream; tnrd_sample_speckle)")
     return ap
 
 
@@ -52,7 +55,8 @@ def _despeckle(a) -> int:
 
 
 def _simulate(a) -> int:
-    pair = sample_speckle(tio.load_image(a.input), SpeckleConfig(looks=a.looks, seed=a.seed))
+    sampler = sample_speckle_gpu if a.gpu else sample_speckle
+    pair = sampler(tio.load_image(a.input), SpeckleConfig(looks=a.looks, seed=a.seed))
     tio.save_image(pair.noisy, a.output, peak=a.peak)
     return 0
 

@@ -22,6 +22,7 @@
 #include "tnrd_stage.cuh"
 #include "tnrd_stage_tc.cuh"
 #include "tnrd_stage_tc3.cuh"
+#include "tnrd_speckle.cuh"
 
 using namespace tnrd;
 
@@ -954,6 +955,46 @@ extern "C" __attribute__((visibility("default"))) int tnrd_debug_split_trace(uns
     return TNRD_OK;
 }
 #endif
+
+// ----------------------------------------------------------------- speckle
+
+// speckle.py:51-70 (statistical parity; tnrd_speckle.cuh)
+extern "C" int tnrd_sample_speckle(const float* clean, float* out, int batch, int H, int W,
+                                   int64_t ld, int64_t image_stride, int looks, uint64_t seed,
+                                   uint32_t* d_status, void* stream) {
+    if (!out) return fail(TNRD_EINVAL, "NULL buffer");
+    if (looks < 1) return fail(TNRD_EINVAL, "looks must be >= 1, got %d", looks);
+    if (batch < 1 || H < 1 || W < 1) return fail(TNRD_EINVAL, "empty image");
+    if (ld < W) return fail(TNRD_EINVAL, "row stride %lld < width %d", (long long)ld, W);
+    if (batch > 1 && image_stride < ld * H)
+        return fail(TNRD_EINVAL, "image stride %lld too small", (long long)image_stride);
+    SpeckleArgs a;
+    a.clean = clean;
+    a.out = out;
+    a.ld = ld;
+    a.img_stride = image_stride;
+    a.H = H; a.W = W; a.batch = batch;
+    a.k0 = (uint32_t)seed;
+    a.k1 = (uint32_t)(seed >> 32);
+    const double d = looks - 1.0 / 3.0;
+    a.d = (float)d;
+    a.c = (float)(1.0 / std::sqrt(9.0 * d));
+    a.inv_l = (float)(1.0 / looks);
+    a.status = d_status;
+    if (batch > 65535) return fail(TNRD_EINVAL, "batch must be <= 65535");
+    dim3 grid((W + 255) / 256, std::min(H, 65535), batch);
+    speckle_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    g_launches.fetch_add(1);
+    return TNRD_OK;
+}
+
+// host restatement of the generator's integer core, for known-answer tests
+// (no GPU needed): Philox4x32-10 of (counter, key)
+extern "C" void tnrd_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    const Philox4 r = philox4x32_10(Philox4{ctr[0], ctr[1], ctr[2], ctr[3]}, key[0], key[1]);
+    out[0] = r.x; out[1] = r.y; out[2] = r.z; out[3] = r.w;
+}
 
 // ----------------------------------------------------------------- conv2d / prox
 
