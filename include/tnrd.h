@@ -18,6 +18,9 @@
  *                            reference's only calling convention)
  *   tnrd_conv2d           <- conv2d                   (imageops.py:53-72)
  *   tnrd_prox_idiv        <- prox_idiv                (speckle.py:111-121)
+ *   tnrd_stage_backward   <- _stage_backward          (training.py:69-123)
+ *   tnrd_conv2d_adjoint   <- conv2d_adjoint           (imageops.py:75-106)
+ *   tnrd_patch_correlation<- patch_correlation        (imageops.py:109-127)
  *   tnrd_sample_speckle   <- sample_speckle/speckle_field (speckle.py:51-70),
  *                            statistical parity (own counter-based generator)
  *
@@ -156,6 +159,27 @@ float* tnrd_plan_u_device(tnrd_plan* plan);
 
 /* Same-size true convolution with half-sample mirror padding (conv2d,
  * imageops.py:53-72); k: m*m float64 host array, m odd, m <= 15. */
+/* ---- training backward ---------------------------
+ * One stage of training.py:69-123 (_stage_backward) on a dense H x W image:
+ * device u_prev, f, g_next (= dL/du_next; NULL = zero), g_prev (device out,
+ * may be NULL); host outputs (each may be NULL): grad_beta (scalar),
+ * grad_k[nk][m*m] = the kernel-space gradient gk_i (training.py:108-109;
+ * the caller maps it to coefficients with basis^T like training.py:110),
+ * grad_w[nk][M].  Works for both reaction variants.  Synchronous; bit-
+ * reproducible (fixed-order float64 reductions). */
+int tnrd_stage_backward(const tnrd_model* model, int t, const float* u_prev,
+                        const float* f, const float* g_next, float* g_prev,
+                        int H, int W, double* grad_beta, double* grad_k,
+                        double* grad_w, void* stream);
+/* imageops.py:75-106: exact transpose of conv2d(., k) (mirror padded),
+ * dense device images; k is m x m float64 (row-major). */
+int tnrd_conv2d_adjoint(const float* img, float* out, int H, int W,
+                        const double* k, int m, void* stream);
+/* imageops.py:109-127: C[a][b] = sum_P pad(base)[P + (a, b)] adj[P], dense
+ * device images, out = host m x m float64.  Synchronous. */
+int tnrd_patch_correlation(const float* base, const float* adj, int H, int W,
+                           int m, double* out, void* stream);
+
 /* L-look amplitude speckle on the GPU (speckle.py:51-70, SURVEY §8(f) rank
  * 3): out = clean * sqrt(G / L), G ~ Gamma(L, 1) per pixel; clean == NULL
  * writes the field sqrt(G / L) itself.  Generator: Philox4x32-10 keyed by

@@ -11,7 +11,8 @@ from .diffusion import (VARIANTS, DiffusionModel, StageParams, StageTrace,
                         projection_reaction, run_diffusion, run_diffusion_batch,
                         smooth_max, zero_mean_basis)
 from .engine import DeviceModel, device_model_for
-from .imageops import as_image, as_kernel, conv2d, rotate180
+from .imageops import (as_image, as_kernel, conv2d, conv2d_adjoint, patch_correlation,
+                       rotate180)
 from .influence import RbfGrid
 from .speckle import (F_FLOOR, NoisyPair, SpeckleConfig, prox_idiv,
                       nakagami_mean, sample_speckle, sample_speckle_device,
@@ -25,6 +26,7 @@ __all__ = [
     "run_diffusion_batch", "zero_mean_basis", "smooth_max", "projection_reaction",
     "DeviceModel",
     "device_model_for", "as_image", "as_kernel", "conv2d", "rotate180",
+    "conv2d_adjoint", "patch_correlation",
     "RbfGrid", "F_FLOOR", "NoisyPair", "SpeckleConfig", "prox_idiv",
     "sample_speckle", "speckle_field", "sample_speckle_device",
     "sample_speckle_gpu", "speckle_field_device", "nakagami_mean",

@@ -72,6 +72,10 @@ SIGNATURES = {
     "tnrd_conv2d": (_c_int, [_vp, _vp, _c_int, _c_int, _c_i64, _dp, _c_int,
                              _vp]),
     "tnrd_prox_idiv": (_c_int, [_vp, _vp, _vp, _c_i64, _c_dbl, _vp]),
+    "tnrd_stage_backward": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _vp, _c_int, _c_int,
+                                     ctypes.POINTER(_c_dbl), _dp, _dp, _vp]),
+    "tnrd_conv2d_adjoint": (_c_int, [_vp, _vp, _c_int, _c_int, _dp, _c_int, _vp]),
+    "tnrd_patch_correlation": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _dp, _vp]),
     "tnrd_sample_speckle": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _c_i64,
                                      _c_i64, _c_int, ctypes.c_uint64, _vp, _vp]),
     "tnrd_philox4x32_10": (None, [ctypes.POINTER(_c_u32), ctypes.POINTER(_c_u32),

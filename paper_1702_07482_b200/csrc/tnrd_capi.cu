@@ -23,6 +23,7 @@
 #include "tnrd_stage_tc.cuh"
 #include "tnrd_stage_tc3.cuh"
 #include "tnrd_speckle.cuh"
+#include "tnrd_train.cuh"
 
 using namespace tnrd;
 
@@ -739,15 +740,14 @@ static int check_shape(const tnrd_model* md, int batch, int H, int W, int64_t ld
     return TNRD_OK;
 }
 
-static int launch_stage(const tnrd_model* md, int t, const float* u_in, const float* f,
-                        float* u_out, int batch, int H, int W, int64_t ld, int64_t image_stride,
-                        uint32_t flags, uint32_t* d_status, cudaStream_t s) {
+// stage t's kernel arguments (model tables, RBF and reaction constants)
+static StageArgs stage_args(const tnrd_model* md, int t, uint32_t flags) {
     StageArgs a;
-    a.u_in = u_in; a.f = f; a.u_out = u_out;
+    a.u_in = nullptr; a.f = nullptr; a.u_out = nullptr;
     a.taps = md->d_taps + (size_t)t * md->nk_pad * md->kp;
     a.tab = md->d_tab + (size_t)t * md->nk_pad * md->tab_stride;
-    a.ld = ld; a.img_stride = image_stride;
-    a.H = H; a.W = W;
+    a.ld = 0; a.img_stride = 0;
+    a.H = 0; a.W = 0;
     a.ngroups = round_up(md->nk, kF) / kF;
     a.nk = md->nk;
     a.tab_stride = md->tab_stride;
@@ -773,6 +773,17 @@ static int launch_stage(const tnrd_model* md, int t, const float* u_in, const fl
     if (md->variant == TNRD_VARIANT_PROJECTED) flags |= TNRD_STAGE_PROJECTED;
     a.flags = flags;
     a.stage = t;
+    a.status = nullptr;
+    return a;
+}
+
+static int launch_stage(const tnrd_model* md, int t, const float* u_in, const float* f,
+                        float* u_out, int batch, int H, int W, int64_t ld, int64_t image_stride,
+                        uint32_t flags, uint32_t* d_status, cudaStream_t s) {
+    StageArgs a = stage_args(md, t, flags);
+    a.u_in = u_in; a.f = f; a.u_out = u_out;
+    a.ld = ld; a.img_stride = image_stride;
+    a.H = H; a.W = W;
     a.status = d_status;
     const int mode = g_kernel_mode.load();
     if (mode == 2 && tc3_supported(md)) return dispatch_tc3(md, t, a, batch, s);
@@ -955,6 +966,176 @@ extern "C" __attribute__((visibility("default"))) int tnrd_debug_split_trace(uns
     return TNRD_OK;
 }
 #endif
+
+// ----------------------------------------------------------------- training backward
+
+// stream-ordered scratch freed on scope exit (after the caller's sync)
+struct StreamScratch {
+    cudaStream_t s;
+    std::vector<void*> ptrs;
+    explicit StreamScratch(cudaStream_t st) : s(st) {}
+    template <class T>
+    cudaError_t get(T** p, size_t count) {
+        void* q = nullptr;
+        cudaError_t e = cudaMallocAsync(&q, std::max<size_t>(count, 1) * sizeof(T), s);
+        if (e == cudaSuccess) ptrs.push_back(q);
+        *p = static_cast<T*>(q);
+        return e;
+    }
+    ~StreamScratch() {
+        for (void* q : ptrs) cudaFreeAsync(q, s);
+    }
+};
+
+// training.py:69-123 (_stage_backward) for one dense H x W image on the GPU
+// (tnrd_train.cuh).  Device inputs u_prev, f, g_next (NULL = zero adjoint);
+// g_prev: device output (NULL: not wanted).  Host outputs (NULL: not
+// wanted): *grad_beta, grad_k[nk][m*m] (the kernel-space gradient gk_i of
+// training.py:108-110, before the basis map), grad_w[nk][M].  Synchronous.
+extern "C" int tnrd_stage_backward(const tnrd_model* md, int t, const float* u_prev, const float* f,
+                                   const float* g_next, float* g_prev, int H, int W,
+                                   double* grad_beta, double* grad_k, double* grad_w, void* stream) {
+    if (!md) return fail(TNRD_EINVAL, "model is NULL");
+    if (t < 0 || t >= md->T) return fail(TNRD_EINVAL, "stage %d out of range [0, %d)", t, md->T);
+    if (!u_prev || !f) return fail(TNRD_EINVAL, "NULL buffer");
+    int rc = check_shape(md, 1, H, W, W, (int64_t)W * H);
+    if (rc) return rc;
+    DeviceGuard dg(md->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int n = H * W;
+    const int m = md->m, mm = m * m, M = md->M, nk = md->nk;
+    const int nout = 2 * mm + M;
+    const int nfc = std::min(nk, 16);
+    const int nblk = (n + train::kRedPx - 1) / train::kRedPx;
+    const bool want_params = grad_beta || grad_k || grad_w;
+    StreamScratch scr(s);
+    float *force, *g_t, *z, *phi, *dphi, *v, *w1, *gp;
+    double *part, *outd;
+    uint32_t* status;
+    const size_t maps = (size_t)nfc * n;
+    if (scr.get(&force, n) || scr.get(&g_t, n) || scr.get(&z, maps) || scr.get(&phi, maps) ||
+        scr.get(&dphi, maps) || scr.get(&v, maps) || scr.get(&w1, maps) || scr.get(&gp, n) ||
+        scr.get(&part, std::max<size_t>((size_t)nfc * nblk * nout, (size_t)nblk)) ||
+        scr.get(&outd, (size_t)nfc * nout) || scr.get(&status, TNRD_STATUS_WORDS))
+        return fail(TNRD_ECUDA, "backward workspace allocation failed");
+    rc = tnrd_status_reset(status, s);
+    if (rc) return rc;
+    // force(u_prev) by the fused stage kernel (TNRD_STAGE_FORCE)
+    rc = launch_stage(md, t, u_prev, f, force, 1, H, W, W, (int64_t)W * H, TNRD_STAGE_FORCE, status, s);
+    if (rc) return rc;
+
+    train::BwdArgs a;
+    a.s = stage_args(md, t, 0u);
+    a.H = H; a.W = W; a.m = m; a.kp = md->kp;
+    a.u = u_prev; a.f = f; a.force = force; a.g_next = g_next;
+    a.g_t = g_t; a.z = z; a.phi = phi; a.dphi = dphi; a.v = v; a.w1 = w1;
+    a.g_prev = g_prev ? g_prev : gp;
+    a.part = part;
+    a.nblk = nblk;
+    a.projected = md->variant == TNRD_VARIANT_PROJECTED;
+    a.f0 = 0; a.nf = nfc; a.last_chunk = 0;
+    const unsigned pblocks = (unsigned)((n + 255) / 256);
+    train::bwd_pointwise_kernel<<<pblocks, 256, 0, s>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    g_launches.fetch_add(1);
+    if (grad_beta) {
+        train::bwd_final_kernel<<<1, 32, 0, s>>>(part, outd, 1, (int)pblocks, 1);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(grad_beta, outd, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        g_launches.fetch_add(1);
+    }
+    for (int f0 = 0; f0 < nk; f0 += nfc) {
+        a.f0 = f0;
+        a.nf = std::min(nfc, nk - f0);
+        a.last_chunk = f0 + a.nf >= nk;
+        const dim3 grid(pblocks, (unsigned)a.nf);
+        if (md->fast) train::bwd_maps_kernel<true><<<grid, 256, 0, s>>>(a);
+        else train::bwd_maps_kernel<false><<<grid, 256, 0, s>>>(a);
+        train::bwd_v_kernel<<<grid, 256, 0, s>>>(a);
+        train::bwd_gprev_kernel<<<pblocks, 256, 0, s>>>(a);
+        CUDA_TRY(cudaGetLastError());
+        g_launches.fetch_add(3);
+        if (grad_k || grad_w) {
+            train::bwd_reduce_kernel<<<dim3((unsigned)nblk, (unsigned)a.nf), 128, 0, s>>>(a);
+            const int tot = a.nf * nout;
+            train::bwd_final_kernel<<<(tot + 127) / 128, 128, 0, s>>>(part, outd, a.nf, nblk, nout);
+            CUDA_TRY(cudaGetLastError());
+            g_launches.fetch_add(2);
+            std::vector<double> h((size_t)tot);
+            CUDA_TRY(cudaMemcpyAsync(h.data(), outd, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            for (int fi = 0; fi < a.nf; ++fi) {
+                const double* o = h.data() + (size_t)fi * nout;
+                if (grad_k) {
+                    double* gk = grad_k + (size_t)(f0 + fi) * mm;
+                    // gk = -rot180(C1) - C2 (training.py:108-109)
+                    for (int q = 0; q < mm; ++q) gk[q] = -o[mm - 1 - q] - o[mm + q];
+                }
+                if (grad_w)
+                    for (int j = 0; j < M; ++j) grad_w[(size_t)(f0 + fi) * M + j] = -o[2 * mm + j];
+            }
+        }
+    }
+    (void)want_params;
+    CUDA_TRY(cudaStreamSynchronize(s));
+    uint32_t hs[TNRD_STATUS_WORDS];
+    CUDA_TRY(cudaMemcpy(hs, status, sizeof hs, cudaMemcpyDeviceToHost));
+    int bad = -1;
+    return tnrd_status_decode(hs, &bad);
+}
+
+// imageops.py:75-106 conv2d_adjoint: exact transpose of conv2d(., k) with the
+// half-sample mirror padding, dense H x W device images
+extern "C" int tnrd_conv2d_adjoint(const float* img, float* out, int H, int W, const double* k, int m,
+                                   void* stream) {
+    if (!img || !out || !k) return fail(TNRD_EINVAL, "NULL buffer");
+    if (m < 1 || m % 2 != 1) return fail(TNRD_EINVAL, "kernel side must be odd, got %d", m);
+    if (m > 15) return fail(TNRD_EUNSUPPORTED, "conv2d_adjoint supports m <= 15, got %d", m);
+    if (H < 1 || W < 1) return fail(TNRD_EINVAL, "image must have at least one pixel");
+    if (m > 2 * std::min(H, W) + 1)
+        return fail(TNRD_EINVAL, "kernel size %d degenerate for image of shape (%d, %d)", m, H, W);
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<float> kf((size_t)m * m);
+    for (int i = 0; i < m * m; ++i) {
+        if (!std::isfinite(k[i])) return fail(TNRD_EINVAL, "kernel contains non-finite values");
+        kf[i] = (float)k[i];
+    }
+    StreamScratch scr(s);
+    float* dk;
+    if (scr.get(&dk, kf.size())) return fail(TNRD_ECUDA, "allocation failed");
+    CUDA_TRY(cudaMemcpyAsync(dk, kf.data(), kf.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+    train::conv2d_adjoint_kernel<<<(unsigned)((H * W + 255) / 256), 256, 0, s>>>(img, out, H, W, dk, m);
+    CUDA_TRY(cudaGetLastError());
+    g_launches.fetch_add(1);
+    CUDA_TRY(cudaStreamSynchronize(s));  // kf lives on the host stack
+    return TNRD_OK;
+}
+
+// imageops.py:109-127 patch_correlation: C[a][b] = sum_P pad(base)[P + (a, b)]
+// adj[P] (symmetric pad by m/2), dense H x W device images; out: host m x m
+// float64.  Synchronous; two-pass fixed-order reduction.
+extern "C" int tnrd_patch_correlation(const float* base, const float* adj, int H, int W, int m,
+                                      double* out, void* stream) {
+    if (!base || !adj || !out) return fail(TNRD_EINVAL, "NULL buffer");
+    if (m < 1 || m % 2 != 1) return fail(TNRD_EINVAL, "kernel side must be odd, got %d", m);
+    if (H < 1 || W < 1) return fail(TNRD_EINVAL, "image must have at least one pixel");
+    if (m > 2 * std::min(H, W) + 1)
+        return fail(TNRD_EINVAL, "kernel size %d degenerate for image of shape (%d, %d)", m, H, W);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int n = H * W, mm = m * m;
+    const int nblk = (n + train::kRedPx - 1) / train::kRedPx;
+    StreamScratch scr(s);
+    double *part, *outd;
+    if (scr.get(&part, (size_t)nblk * mm) || scr.get(&outd, mm)) return fail(TNRD_ECUDA, "allocation failed");
+    train::patch_corr_kernel<<<nblk, 128, 0, s>>>(base, adj, H, W, m, part);
+    train::bwd_final_kernel<<<(mm + 127) / 128, 128, 0, s>>>(part, outd, 1, nblk, mm);
+    CUDA_TRY(cudaGetLastError());
+    g_launches.fetch_add(2);
+    CUDA_TRY(cudaMemcpyAsync(out, outd, mm * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return TNRD_OK;
+}
 
 // ----------------------------------------------------------------- speckle
 

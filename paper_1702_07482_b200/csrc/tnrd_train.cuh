@@ -1,0 +1,322 @@
+// tnrd_train.cuh -- stage backward of the TNRD diffusion on the GPU (SURVEY
+// §8(f) rank 4: training.py:69-123 `_stage_backward`, imageops.py:75-127
+// `conv2d_adjoint` / `patch_correlation`).
+//
+// For one stage t with u = u_prev, f, lambda and the upstream adjoint
+// g_next = dL/du_next (reference names):
+//
+//   u~      = u - force(u)                      (prox)   training.py:79-83
+//           = u - force(u) - lam (1/u - f^2/u^3) (projected)
+//   g_t     = y * g_next, y = prox'(u~) or smooth_max'(u~)
+//   grad_beta = lam * sum(dprox/dlam(u~) g_next)        (prox)
+//             = -lam * sum((1/u - f^2/u^3) g_t)        (projected)
+//   for each filter i:
+//     z_i   = conv2d(u, k_i), phi_i = phi_i(z_i), phi'_i(z_i)
+//     v_i   = conv2d_adjoint(g_t, rot180(k_i))
+//     w1_i  = phi'_i * v_i
+//     grad_weights[i][j] = -sum_P G_j(z_i[P]) v_i[P]
+//     gk_i  = -rot180(patch_corr(u, w1_i)) - patch_corr(phi_i, g_t)
+//             (the host maps gk_i to coefficient space: basis^T gk_i)
+//     g_prev -= conv2d_adjoint(w1_i, k_i)          (filters ascending)
+//   g_prev starts at g_t; the projected variant finally subtracts
+//   lam (-1/u^2 + 3 f^2/u^4) g_t.
+//
+// Layout: whole-image maps per filter chunk in a stream-ordered workspace
+// (training images are small: a 512^2 image x 48 filters x 5 maps = 252 MB).
+// Kernels are direct (gather) formulations over the image -- the mirror
+// padding's adjoint is folded in exactly, per output pixel, instead of the
+// reference's full convolution + border fold -- and every reduction is
+// two-pass in a fixed order (per-block partials in float64, then summed in
+// block order), so results are bit-reproducible.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tnrd_stage.cuh"
+
+namespace tnrd {
+namespace train {
+
+// half-sample mirror (one fold)
+__device__ __forceinline__ int mir1(int j, int n) {
+    return j < 0 ? -1 - j : (j >= n ? 2 * n - 1 - j : j);
+}
+
+// phi'(z) from the per-filter polynomial table (derivative of rbf_poly's
+// interpolant: p'(x) / h)
+__device__ __forceinline__ float rbf_poly_deriv(float z, const float* __restrict__ tabf,
+                                                const StageArgs& p) {
+    float t = fmaf(z, p.inv_h, p.t_off);
+    t = fminf(fmaxf(t, 0.0f), p.tmax);
+    const float r = t + 12582912.0f;
+    const int j = __float_as_int(r) - 0x4B400000;
+    const float x = t - (r - 12582912.0f);
+    const int sw = (j >> 2) & 1;
+    const float* c = tabf + j * kPolyN;
+    const float4 lo = *reinterpret_cast<const float4*>(c + 4 * sw);
+    const float4 hi = *reinterpret_cast<const float4*>(c + 4 * (sw ^ 1));
+    float acc = fmaf(7.0f * hi.w, x, 6.0f * hi.z);
+    acc = fmaf(acc, x, 5.0f * hi.y);
+    acc = fmaf(acc, x, 4.0f * hi.x);
+    acc = fmaf(acc, x, 3.0f * lo.w);
+    acc = fmaf(acc, x, 2.0f * lo.z);
+    acc = fmaf(acc, x, lo.y);
+    return acc * p.inv_h;
+}
+
+// phi'(z) as the reference writes it (influence.py:48-54 / training.py:90-94):
+// sum_j w_j G_j(z) (mu_j - z) / gamma^2
+__device__ __forceinline__ float rbf_direct_deriv(float z, const float* __restrict__ w,
+                                                  const StageArgs& p) {
+    const float inv_g2 = -2.0f * p.cE / 1.4426950408889634f;
+    float s = 0.0f;
+    for (int j = 0; j < p.M; ++j) {
+        const float mu = fmaf((float)j, p.delta, p.mu0);
+        const float d = z - mu;
+        s = fmaf(w[j] * ex2f(d * d * p.cE), -d, s);
+    }
+    return s * inv_g2;
+}
+
+struct BwdArgs {
+    StageArgs s;          // model tables of the stage (taps, tab, RBF constants, lam, variant)
+    int H, W;             // dense images (ld = W)
+    int m, kp;            // filter side, floats per filter in taps
+    int f0, nf;           // filter chunk [f0, f0 + nf)
+    const float* u;       // u_prev
+    const float* f;       // observation
+    const float* force;   // force(u_prev)
+    const float* g_next;  // dL/du_next (NULL = zero)
+    float* g_t;           // [H*W]
+    float* z;             // [nf][H*W]
+    float* phi;
+    float* dphi;
+    float* v;
+    float* w1;
+    float* g_prev;        // [H*W] in/out across chunks
+    double* part;         // reduction partials
+    int nblk;             // pixel blocks of the reductions
+    int projected;
+    int last_chunk;
+};
+
+constexpr int kRedPx = 256;  // pixels per reduction block
+
+// g_t and the beta partials (per 256-pixel block, float64)
+__global__ void __launch_bounds__(256) bwd_pointwise_kernel(const BwdArgs a) {
+    __shared__ double red[256];
+    const int n = a.H * a.W;
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    double contrib = 0.0;
+    if (i < n) {
+        const float u = a.u[i], fv = a.f[i];
+        const float gn = a.g_next ? a.g_next[i] : 0.0f;
+        const float lam = a.s.lam;
+        float gt;
+        // the pointwise derivatives are evaluated in float64: the reference
+        // formulas cancel (dprox/dlam subtracts two terms of similar size;
+        // 1/u - f^2/u^3 vanishes at f = u), and the beta gradient sums them
+        // over the image with further cancellation
+        const double ud = u, fd = fv, ld = lam;
+        if (a.projected) {
+            const double rr = 1.0 / ud - (fd * fd) / (ud * ud * ud);
+            const float ut = u - a.force[i] - (float)(ld * rr);
+            const float tt = (ut - a.s.pfloor) * a.s.inv_tau;
+            // stable logistic (diffusion.py:159-168)
+            const float y = tt >= 0.0f ? 1.0f / (1.0f + expf(-tt)) : expf(tt) / (1.0f + expf(tt));
+            gt = y * gn;
+            contrib = -ld * rr * (double)gt;
+        } else {
+            const double ff = fmax(fd, (double)kFFloor);
+            const double ut = (double)(u - a.force[i]);
+            const double aa = 1.0 + 2.0 * ld;
+            const double root = sqrt(ut * ut + 8.0 * aa * ld * ff * ff);
+            const double y = (1.0 + ut / root) / (2.0 * aa);           // speckle.py:123-128
+            const double x = (2.0 * ff * ff + 8.0 * ld * ff * ff) / (aa * root) -
+                             (ut + root) / (aa * aa);                  // speckle.py:131-137
+            gt = (float)(y * (double)gn);
+            contrib = ld * x * (double)gn;
+        }
+        a.g_t[i] = gt;
+    }
+    red[threadIdx.x] = contrib;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) a.part[blockIdx.x] = red[0];
+}
+
+// z, phi, phi' of the chunk's filters (true convolution, mirror padded)
+template <bool FAST>
+__global__ void __launch_bounds__(256) bwd_maps_kernel(const BwdArgs a) {
+    const int n = a.H * a.W;
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    const int fi = blockIdx.y;
+    if (i >= n) return;
+    const int Y = i / a.W, X = i - Y * a.W;
+    const int r = a.m / 2;
+    const int gf = a.f0 + fi;
+    const float* k = a.s.taps + (size_t)gf * a.kp;
+    float z = 0.0f;
+    for (int p = -r; p <= r; ++p) {
+        const float* row = a.u + (size_t)mir1(Y - p, a.H) * a.W;
+        for (int q = -r; q <= r; ++q) z = fmaf(k[(r + p) * a.m + r + q], __ldg(row + mir1(X - q, a.W)), z);
+    }
+    const float* tab = a.s.tab + (size_t)gf * a.s.tab_stride;
+    const size_t o = (size_t)fi * n + i;
+    a.z[o] = z;
+    a.phi[o] = FAST ? rbf_poly(z, tab, a.s) : rbf_direct(z, tab, a.s);
+    a.dphi[o] = FAST ? rbf_poly_deriv(z, tab, a.s) : rbf_direct_deriv(z, tab, a.s);
+}
+
+// (conv2d(., K)^T img)[Y, X] = sum_{p,q} K[r+p][r+q] sum over the preimages
+// y of Y under y -> mir(y - p) (and likewise for x) of img[y][x]
+__device__ __forceinline__ int preimages(int Y, int p, int n, int* out) {
+    int c = 0;
+    const int y0 = Y + p;                  // direct
+    if (y0 >= 0 && y0 < n) out[c++] = y0;
+    const int y1 = p - 1 - Y;              // mirrored below 0: y - p = -1 - Y
+    if (y1 >= 0 && y1 < n) out[c++] = y1;
+    const int y2 = 2 * n - 1 - Y + p;      // mirrored above n: y - p = 2n - 1 - Y
+    if (y2 >= 0 && y2 < n) out[c++] = y2;
+    return c;
+}
+
+// K[r+p][r+q] = kflip ? k[r-p][r-q] : k[r+p][r+q]
+__device__ __forceinline__ float adjoint_at(const float* __restrict__ img, int H, int W, int Y, int X,
+                                            const float* k, int m, bool kflip) {
+    const int r = m / 2;
+    float s = 0.0f;
+    for (int p = -r; p <= r; ++p) {
+        int ys[3];
+        const int ny = preimages(Y, p, H, ys);
+        for (int q = -r; q <= r; ++q) {
+            int xs[3];
+            const int nx = preimages(X, q, W, xs);
+            const float kk = kflip ? k[(r - p) * m + (r - q)] : k[(r + p) * m + (r + q)];
+            float t = 0.0f;
+            for (int a = 0; a < ny; ++a)
+                for (int b = 0; b < nx; ++b) t += __ldg(img + (size_t)ys[a] * W + xs[b]);
+            s = fmaf(kk, t, s);
+        }
+    }
+    return s;
+}
+
+// v_i = conv2d_adjoint(g_t, rot180(k_i)), w1_i = phi'_i v_i
+__global__ void __launch_bounds__(256) bwd_v_kernel(const BwdArgs a) {
+    const int n = a.H * a.W;
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    const int fi = blockIdx.y;
+    if (i >= n) return;
+    const int Y = i / a.W, X = i - Y * a.W;
+    const float* k = a.s.taps + (size_t)(a.f0 + fi) * a.kp;
+    const float v = adjoint_at(a.g_t, a.H, a.W, Y, X, k, a.m, true);
+    const size_t o = (size_t)fi * n + i;
+    a.v[o] = v;
+    a.w1[o] = a.dphi[o] * v;
+}
+
+// g_prev -= conv2d_adjoint(w1_i, k_i) over the chunk's filters, ascending;
+// the first chunk starts from g_t, the last adds the projected reaction term
+__global__ void __launch_bounds__(256) bwd_gprev_kernel(const BwdArgs a) {
+    const int n = a.H * a.W;
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= n) return;
+    const int Y = i / a.W, X = i - Y * a.W;
+    float g = a.f0 == 0 ? a.g_t[i] : a.g_prev[i];
+    for (int fi = 0; fi < a.nf; ++fi) {
+        const float* k = a.s.taps + (size_t)(a.f0 + fi) * a.kp;
+        g -= adjoint_at(a.w1 + (size_t)fi * n, a.H, a.W, Y, X, k, a.m, false);
+    }
+    if (a.last_chunk && a.projected) {
+        const float u = a.u[i], fv = a.f[i];
+        g -= a.s.lam * (-1.0f / (u * u) + 3.0f * fv * fv / (u * u * u * u)) * a.g_t[i];
+    }
+    a.g_prev[i] = g;
+}
+
+// per (filter, 256-pixel block) partial sums, float64, one output per thread:
+//   o <  m^2       : C1[o] = sum_P u[mir(P + off(o))] w1[P]
+//   o <  2 m^2     : C2[o - m^2] = sum_P phi[mir(P + off)] g_t[P]
+//   o <  2 m^2 + M : GW[j] = sum_P G_j(z[P]) v[P]
+// with off(a, b) = (a - r, b - r) (patch_correlation, imageops.py:109-127;
+// phi is mirror padded through mir exactly like np.pad symmetric)
+__global__ void __launch_bounds__(256) bwd_reduce_kernel(const BwdArgs a) {
+    const int n = a.H * a.W;
+    const int fi = blockIdx.y, blk = blockIdx.x;
+    const int mm = a.m * a.m, nout = 2 * mm + a.s.M;
+    const int r = a.m / 2;
+    const int P0 = blk * kRedPx, P1 = min(n, P0 + kRedPx);
+    const size_t fo = (size_t)fi * n;
+    const float inv_2g2 = a.s.cE;  // -log2(e) / (2 gamma^2): G = exp2(d^2 cE)
+    for (int o = threadIdx.x; o < nout; o += blockDim.x) {
+        double acc = 0.0;
+        if (o < 2 * mm) {
+            const bool second = o >= mm;
+            const int oo = second ? o - mm : o;
+            const int da = oo / a.m - r, db = oo % a.m - r;
+            const float* base = second ? a.phi + fo : a.u;
+            const float* adj = second ? a.g_t : a.w1 + fo;
+            float s = 0.0f;
+            for (int P = P0; P < P1; ++P) {
+                const int Y = P / a.W, X = P - Y * a.W;
+                s = fmaf(__ldg(base + (size_t)mir1(Y + da, a.H) * a.W + mir1(X + db, a.W)), __ldg(adj + P), s);
+            }
+            acc = s;
+        } else {
+            const int j = o - 2 * mm;
+            const float mu = fmaf((float)j, a.s.delta, a.s.mu0);
+            float s = 0.0f;
+            for (int P = P0; P < P1; ++P) {
+                const float d = __ldg(a.z + fo + P) - mu;
+                s = fmaf(ex2f(d * d * inv_2g2), __ldg(a.v + fo + P), s);
+            }
+            acc = s;
+        }
+        a.part[((size_t)fi * a.nblk + blk) * nout + o] = acc;
+    }
+}
+
+// sum partials over blocks in block order: out[i][o] = sum_b part[i][b][o]
+__global__ void bwd_final_kernel(const double* __restrict__ part, double* out, int nf, int nblk, int nout) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nf * nout) return;
+    const int fi = t / nout, o = t - fi * nout;
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += part[((size_t)fi * nblk + b) * nout + o];
+    out[t] = s;
+}
+
+// drop-in conv2d_adjoint (imageops.py:90-106) for one kernel
+__global__ void __launch_bounds__(256) conv2d_adjoint_kernel(const float* __restrict__ img, float* out,
+                                                            int H, int W, const float* k, int m) {
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= H * W) return;
+    const int Y = i / W, X = i - Y * W;
+    out[i] = adjoint_at(img, H, W, Y, X, k, m, false);
+}
+
+// drop-in patch_correlation (imageops.py:109-127): per 256-pixel block
+// partials of C[a][b] = sum_P base[mir(P + (a - r, b - r))] adj[P]
+__global__ void __launch_bounds__(128) patch_corr_kernel(const float* __restrict__ base,
+                                                        const float* __restrict__ adj, int H, int W,
+                                                        int m, double* part) {
+    const int n = H * W, mm = m * m, r = m / 2;
+    const int blk = blockIdx.x;
+    const int P0 = blk * kRedPx, P1 = min(n, P0 + kRedPx);
+    for (int o = threadIdx.x; o < mm; o += blockDim.x) {
+        const int da = o / m - r, db = o % m - r;
+        float s = 0.0f;
+        for (int P = P0; P < P1; ++P) {
+            const int Y = P / W, X = P - Y * W;
+            s = fmaf(__ldg(base + (size_t)mir1(Y + da, H) * W + mir1(X + db, W)), __ldg(adj + P), s);
+        }
+        part[(size_t)blk * mm + o] = s;
+    }
+}
+
+}  // namespace train
+}  // namespace tnrd

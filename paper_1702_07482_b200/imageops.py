@@ -70,3 +70,45 @@ def conv2d(img, k, method: str = "auto") -> np.ndarray:
                                        _lib.dptr(kk), k.shape[0],
                                        _stream_handle()))
     return out.cpu().numpy().astype(np.float64)
+
+
+def conv2d_adjoint(img, k, method: str = "auto") -> np.ndarray:
+    """Exact transpose of ``conv2d(., k)`` (imageops.py:90-106): satisfies
+    <conv2d(a, k), b> == <a, conv2d_adjoint(b, k)>.  GPU, fp32 (the mirror
+    padding's adjoint is folded per output pixel); returns float64."""
+    img = as_image(img)
+    k = as_kernel(k)
+    check_fits(img.shape, k.shape[0])
+    if method not in ("auto", "direct", "fft"):
+        raise ValueError(f"unknown convolution method {method!r}")
+    require_cuda()
+    t = torch()
+    H, W = img.shape
+    x = t.from_numpy(img.astype(np.float32)).cuda()
+    out = t.empty_like(x)
+    kk = np.ascontiguousarray(k)
+    _lib.check(_lib.load().tnrd_conv2d_adjoint(_ptr(x), _ptr(out), H, W, _lib.dptr(kk),
+                                               k.shape[0], _stream_handle()))
+    return out.cpu().numpy().astype(np.float64)
+
+
+def patch_correlation(base, adj, m: int) -> np.ndarray:
+    """C[a, b] = sum_p pad(base)[p + (a, b)] adj[p] with pad = symmetric
+    padding by m // 2 (imageops.py:109-127); rotate180(C) is the gradient of
+    <adj, conv2d(base, k)> w.r.t. k.  GPU, fp32 products, float64 sums."""
+    base = as_image(base, "base")
+    adj = as_image(adj, "adj")
+    if base.shape != adj.shape:
+        raise ValueError("base and adj must share dimensions")
+    if m < 1 or m % 2 != 1:
+        raise ValueError(f"kernel side must be odd, got {m}")
+    check_fits(base.shape, m)
+    require_cuda()
+    t = torch()
+    H, W = base.shape
+    b = t.from_numpy(base.astype(np.float32)).cuda()
+    a = t.from_numpy(adj.astype(np.float32)).cuda()
+    out = np.empty((m, m), dtype=np.float64)
+    _lib.check(_lib.load().tnrd_patch_correlation(_ptr(b), _ptr(a), H, W, m, _lib.dptr(out),
+                                                  _stream_handle()))
+    return out

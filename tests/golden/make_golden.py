@@ -157,6 +157,47 @@ def main(which):
              pgm16=sdio.load_image(os.path.join(HERE, "io_image16.pgm")),
              **pack_model(model))
         print("wrote io fixtures")
+    if "training" in which:
+        # training.py:69-166 gradients of the real reference (rank 4 of
+        # SURVEY 8(f)); inputs are fp32-exact so the GPU sees the same data
+        from specklediff import training as sdt
+        from specklediff.imageops import conv2d_adjoint, patch_correlation
+        from specklediff.speckle import SpeckleConfig, sample_speckle
+        trng = np.random.default_rng(777)
+        out = {}
+        cases = [("p_m3_nk2_T1", 3, 2, 1, 5, (8, 8), "prox"),
+                 ("p_m5_nk6_T2", 5, 6, 2, 63, (19, 23), "prox"),
+                 ("p_m7_nk20_T2", 7, 20, 2, 63, (33, 29), "prox"),
+                 ("q_m3_nk3_T2", 3, 3, 2, 7, (12, 10), "projected"),
+                 ("q_m5_nk5_T1", 5, 5, 1, 63, (17, 21), "projected")]
+        for ci, (name, m, nk, T, M, shape, variant) in enumerate(cases):
+            model = ref_model(m, nk, T, M, seed=500 + ci, weight_scale=0.3,
+                              variant=variant, betas=list(0.3 * trng.standard_normal(T)))
+            clean = np.float32(trng.uniform(20.0, 235.0, size=shape)).astype(np.float64)
+            noisy = np.float32(sample_speckle(clean, SpeckleConfig(looks=4, seed=7)).noisy).astype(np.float64)
+            pair = sample_speckle(clean, SpeckleConfig(looks=4, seed=7))
+            pair = type(pair)(clean=clean, noisy=noisy, config=pair.config)
+            total, acc = sdt.loss_and_gradients(model, [pair], list(range(T)), T - 1)
+            _, traces = sdt._forward(model, noisy, T - 1, 0)
+            gn = np.float32(trng.normal(size=shape)).astype(np.float64)
+            g_prev, grads = sdt._stage_backward(traces[T - 1], model.stages[T - 1], noisy, gn, model)
+            rec = dict(pack_model(model), clean=clean, noisy=noisy, loss=total, g_next=gn,
+                       g_prev=g_prev, sb_beta=grads.beta, sb_coeffs=grads.coeffs,
+                       sb_weights=grads.weights, u_prev=traces[T - 1].u_prev)
+            for t in range(T):
+                rec[f"beta_{t}"] = acc[t].beta
+                rec[f"coeffs_{t}"] = acc[t].coeffs
+                rec[f"weights_{t}"] = acc[t].weights
+            save(f"train_{name}", **rec)
+        img = np.float32(trng.normal(size=(14, 11))).astype(np.float64)
+        adj = np.float32(trng.normal(size=(14, 11))).astype(np.float64)
+        for m in (1, 3, 5, 7, 9):
+            k = trng.normal(size=(m, m))
+            out[f"k{m}"] = k
+            out[f"adj{m}"] = conv2d_adjoint(img, k)
+            out[f"pc{m}"] = patch_correlation(img, adj, m)
+        save("train_imageops", img=img, adj=adj, **out)
+        print("wrote training fixtures")
     for key in ("c1", "c2"):
         if key in which:
             cfg = synth.CONFIGS[key]
@@ -166,4 +207,4 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["small", "projected", "io", "c1", "c2"])
+    main(sys.argv[1:] or ["small", "projected", "io", "training", "c1", "c2"])
