@@ -987,6 +987,34 @@ struct StreamScratch {
     }
 };
 
+// the image-space backward kernels of one filter chunk, each as an interior
+// launch and a border-band launch
+template <int MS>
+static void bwd_image_kernels(const tnrd_model* md, const train::BwdArgs& a, int H, int W, bool gprev,
+                              cudaStream_t s) {
+    for (int pass = 0; pass < 3; ++pass) {
+        if (pass == 2 && !gprev) break;
+        for (int part_i = 0; part_i < 2; ++part_i) {
+            const train::PixelSet ps = train::pixel_set(H, W, MS / 2, part_i == 0);
+            if (ps.n == 0) continue;
+            const dim3 grid((unsigned)((ps.n + 255) / 256), (unsigned)a.nf);
+            if (pass == 0) {
+                if (md->fast) train::bwd_maps_kernel<MS, true><<<grid, 256, 0, s>>>(a, ps);
+                else train::bwd_maps_kernel<MS, false><<<grid, 256, 0, s>>>(a, ps);
+            } else if (pass == 1) {
+                train::bwd_v_kernel<MS><<<grid, 256, 0, s>>>(a, ps);
+            } else {
+                train::bwd_adj_kernel<MS><<<grid, 256, 0, s>>>(a, ps);
+            }
+            g_launches.fetch_add(1);
+        }
+    }
+    if (gprev) {
+        train::bwd_gprev_kernel<<<(unsigned)((H * W + 255) / 256), 256, 0, s>>>(a);
+        g_launches.fetch_add(1);
+    }
+}
+
 // training.py:69-123 (_stage_backward) for one dense H x W image on the GPU
 // (tnrd_train.cuh).  Device inputs u_prev, f, g_next (NULL = zero adjoint);
 // g_prev: device output (NULL: not wanted).  Host outputs (NULL: not
@@ -1006,16 +1034,18 @@ extern "C" int tnrd_stage_backward(const tnrd_model* md, int t, const float* u_p
     const int m = md->m, mm = m * m, M = md->M, nk = md->nk;
     const int nout = 2 * mm + M;
     const int nfc = std::min(nk, 16);
-    const int nblk = (n + train::kRedPx - 1) / train::kRedPx;
+    const int nseg = (W + train::kSeg - 1) / train::kSeg;
+    const int nblk = H * nseg;                 // bwd_reduce_kernel blocks per filter
     const bool want_params = grad_beta || grad_k || grad_w;
     StreamScratch scr(s);
-    float *force, *g_t, *z, *phi, *dphi, *v, *w1, *gp;
+    float *force, *g_t, *z, *phi, *dphi, *v, *w1, *adjb, *gp;
     double *part, *outd;
     uint32_t* status;
     const size_t maps = (size_t)nfc * n;
     if (scr.get(&force, n) || scr.get(&g_t, n) || scr.get(&z, maps) || scr.get(&phi, maps) ||
-        scr.get(&dphi, maps) || scr.get(&v, maps) || scr.get(&w1, maps) || scr.get(&gp, n) ||
-        scr.get(&part, std::max<size_t>((size_t)nfc * nblk * nout, (size_t)nblk)) ||
+        scr.get(&dphi, maps) || scr.get(&v, maps) || scr.get(&w1, maps) ||
+        (g_prev && scr.get(&adjb, maps)) || scr.get(&gp, n) ||
+        scr.get(&part, std::max<size_t>((size_t)nfc * nblk * nout, (size_t)(n + 255) / 256)) ||
         scr.get(&outd, (size_t)nfc * nout) || scr.get(&status, TNRD_STATUS_WORDS))
         return fail(TNRD_ECUDA, "backward workspace allocation failed");
     rc = tnrd_status_reset(status, s);
@@ -1029,6 +1059,7 @@ extern "C" int tnrd_stage_backward(const tnrd_model* md, int t, const float* u_p
     a.H = H; a.W = W; a.m = m; a.kp = md->kp;
     a.u = u_prev; a.f = f; a.force = force; a.g_next = g_next;
     a.g_t = g_t; a.z = z; a.phi = phi; a.dphi = dphi; a.v = v; a.w1 = w1;
+    a.adj = g_prev ? adjb : nullptr;
     a.g_prev = g_prev ? g_prev : gp;
     a.part = part;
     a.nblk = nblk;
@@ -1039,7 +1070,7 @@ extern "C" int tnrd_stage_backward(const tnrd_model* md, int t, const float* u_p
     CUDA_TRY(cudaGetLastError());
     g_launches.fetch_add(1);
     if (grad_beta) {
-        train::bwd_final_kernel<<<1, 32, 0, s>>>(part, outd, 1, (int)pblocks, 1);
+        train::bwd_final_kernel<<<1, 32, 0, s>>>(part, outd, 1, (int)pblocks, 1);  // one warp
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaMemcpyAsync(grad_beta, outd, sizeof(double), cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
@@ -1049,17 +1080,19 @@ extern "C" int tnrd_stage_backward(const tnrd_model* md, int t, const float* u_p
         a.f0 = f0;
         a.nf = std::min(nfc, nk - f0);
         a.last_chunk = f0 + a.nf >= nk;
-        const dim3 grid(pblocks, (unsigned)a.nf);
-        if (md->fast) train::bwd_maps_kernel<true><<<grid, 256, 0, s>>>(a);
-        else train::bwd_maps_kernel<false><<<grid, 256, 0, s>>>(a);
-        train::bwd_v_kernel<<<grid, 256, 0, s>>>(a);
-        train::bwd_gprev_kernel<<<pblocks, 256, 0, s>>>(a);
+        // interior rectangle and border band as separate launches (uniform warps)
+        switch (m) {
+            case 3: bwd_image_kernels<3>(md, a, H, W, g_prev != nullptr, s); break;
+            case 5: bwd_image_kernels<5>(md, a, H, W, g_prev != nullptr, s); break;
+            case 7: bwd_image_kernels<7>(md, a, H, W, g_prev != nullptr, s); break;
+            default: bwd_image_kernels<9>(md, a, H, W, g_prev != nullptr, s); break;
+        }
         CUDA_TRY(cudaGetLastError());
-        g_launches.fetch_add(3);
         if (grad_k || grad_w) {
-            train::bwd_reduce_kernel<<<dim3((unsigned)nblk, (unsigned)a.nf), 128, 0, s>>>(a);
+            const size_t rsm = sizeof(float) * (2 * (size_t)m * (train::kSeg + 2 * (m / 2)) + 4 * train::kSeg);
+            train::bwd_reduce_kernel<<<dim3((unsigned)nblk, (unsigned)a.nf), 256, rsm, s>>>(a, nseg);
             const int tot = a.nf * nout;
-            train::bwd_final_kernel<<<(tot + 127) / 128, 128, 0, s>>>(part, outd, a.nf, nblk, nout);
+            train::bwd_final_kernel<<<(tot + 3) / 4, 128, 0, s>>>(part, outd, a.nf, nblk, nout);
             CUDA_TRY(cudaGetLastError());
             g_launches.fetch_add(2);
             std::vector<double> h((size_t)tot);
@@ -1129,7 +1162,7 @@ extern "C" int tnrd_patch_correlation(const float* base, const float* adj, int H
     double *part, *outd;
     if (scr.get(&part, (size_t)nblk * mm) || scr.get(&outd, mm)) return fail(TNRD_ECUDA, "allocation failed");
     train::patch_corr_kernel<<<nblk, 128, 0, s>>>(base, adj, H, W, m, part);
-    train::bwd_final_kernel<<<(mm + 127) / 128, 128, 0, s>>>(part, outd, 1, nblk, mm);
+    train::bwd_final_kernel<<<(mm + 3) / 4, 128, 0, s>>>(part, outd, 1, nblk, mm);
     CUDA_TRY(cudaGetLastError());
     g_launches.fetch_add(2);
     CUDA_TRY(cudaMemcpyAsync(out, outd, mm * sizeof(double), cudaMemcpyDeviceToHost, s));

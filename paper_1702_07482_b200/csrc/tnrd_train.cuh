@@ -93,6 +93,7 @@ struct BwdArgs {
     float* dphi;
     float* v;
     float* w1;
+    float* adj;           // [nf][H*W] conv2d_adjoint(w1_i, k_i)
     float* g_prev;        // [H*W] in/out across chunks
     double* part;         // reduction partials
     int nblk;             // pixel blocks of the reductions
@@ -100,7 +101,55 @@ struct BwdArgs {
     int last_chunk;
 };
 
-constexpr int kRedPx = 256;  // pixels per reduction block
+constexpr int kRedPx = 256;  // pixels per reduction block (patch_corr_kernel)
+constexpr int kSeg = 256;    // row-segment width of bwd_reduce_kernel blocks
+
+// Pixel sets of the image-space kernels.  The interior rectangle (every
+// m x m tap window inside the image: no mirror, no fold) runs branch-free;
+// the border band (width r) runs the general mirror / preimage path.  Two
+// launches keep every warp on one path.
+struct PixelSet {
+    int rt, rb, cl, cr;  // band widths: top, bottom, left, right
+    int iw, ih;          // interior rectangle size
+    int n;               // pixels in the set
+    bool interior;
+};
+
+__host__ __device__ inline PixelSet pixel_set(int H, int W, int r, bool interior) {
+    PixelSet ps;
+    ps.rt = min(r, H);
+    ps.rb = min(r, H - ps.rt);
+    ps.cl = min(r, W);
+    ps.cr = min(r, W - ps.cl);
+    ps.ih = H - ps.rt - ps.rb;
+    ps.iw = W - ps.cl - ps.cr;
+    ps.interior = interior;
+    ps.n = interior ? ps.ih * ps.iw : H * W - ps.ih * ps.iw;
+    return ps;
+}
+
+// idx-th pixel of the set -> (Y, X)
+__device__ __forceinline__ void set_pixel(const PixelSet& ps, int W, int idx, int& Y, int& X) {
+    if (ps.interior) {
+        Y = ps.rt + idx / ps.iw;
+        X = ps.cl + idx % ps.iw;
+        return;
+    }
+    const int top = ps.rt * W;
+    if (idx < top) { Y = idx / W; X = idx % W; return; }
+    idx -= top;
+    const int side = ps.cl + ps.cr;
+    const int mid = ps.ih * side;
+    if (idx < mid) {
+        Y = ps.rt + idx / side;
+        const int c = idx % side;
+        X = c < ps.cl ? c : W - ps.cr + (c - ps.cl);
+        return;
+    }
+    idx -= mid;
+    Y = ps.rt + ps.ih + idx / W;
+    X = idx % W;
+}
 
 // g_t and the beta partials (per 256-pixel block, float64)
 __global__ void __launch_bounds__(256) bwd_pointwise_kernel(const BwdArgs a) {
@@ -149,20 +198,31 @@ __global__ void __launch_bounds__(256) bwd_pointwise_kernel(const BwdArgs a) {
 }
 
 // z, phi, phi' of the chunk's filters (true convolution, mirror padded)
-template <bool FAST>
-__global__ void __launch_bounds__(256) bwd_maps_kernel(const BwdArgs a) {
+template <int MS, bool FAST>
+__global__ void __launch_bounds__(256) bwd_maps_kernel(const BwdArgs a, const PixelSet ps) {
     const int n = a.H * a.W;
-    const int i = blockIdx.x * 256 + threadIdx.x;
+    const int idx = blockIdx.x * 256 + threadIdx.x;
     const int fi = blockIdx.y;
-    if (i >= n) return;
-    const int Y = i / a.W, X = i - Y * a.W;
-    const int r = a.m / 2;
+    if (idx >= ps.n) return;
+    int Y, X;
+    set_pixel(ps, a.W, idx, Y, X);
+    const int i = Y * a.W + X;
+    constexpr int r = MS / 2;
     const int gf = a.f0 + fi;
     const float* k = a.s.taps + (size_t)gf * a.kp;
     float z = 0.0f;
-    for (int p = -r; p <= r; ++p) {
-        const float* row = a.u + (size_t)mir1(Y - p, a.H) * a.W;
-        for (int q = -r; q <= r; ++q) z = fmaf(k[(r + p) * a.m + r + q], __ldg(row + mir1(X - q, a.W)), z);
+    if (ps.interior) {
+#pragma unroll
+        for (int p = -r; p <= r; ++p) {
+            const float* row = a.u + (size_t)(Y - p) * a.W + X;
+#pragma unroll
+            for (int q = -r; q <= r; ++q) z = fmaf(k[(r + p) * MS + r + q], __ldg(row - q), z);
+        }
+    } else {
+        for (int p = -r; p <= r; ++p) {
+            const float* row = a.u + (size_t)mir1(Y - p, a.H) * a.W;
+            for (int q = -r; q <= r; ++q) z = fmaf(k[(r + p) * MS + r + q], __ldg(row + mir1(X - q, a.W)), z);
+        }
     }
     const float* tab = a.s.tab + (size_t)gf * a.s.tab_stride;
     const size_t o = (size_t)fi * n + i;
@@ -189,6 +249,16 @@ __device__ __forceinline__ float adjoint_at(const float* __restrict__ img, int H
                                             const float* k, int m, bool kflip) {
     const int r = m / 2;
     float s = 0.0f;
+    if (Y >= r && Y < H - r && X >= r && X < W - r) {
+        // interior: every tap has exactly its direct preimage (Y + p, X + q)
+        const float* base = img + (size_t)(Y - r) * W + (X - r);
+        for (int a = 0; a < m; ++a) {
+            const float* row = base + (size_t)a * W;
+            const float* krow = kflip ? k + (m - 1 - a) * m : k + a * m;
+            for (int b = 0; b < m; ++b) s = fmaf(kflip ? krow[m - 1 - b] : krow[b], __ldg(row + b), s);
+        }
+        return s;
+    }
     for (int p = -r; p <= r; ++p) {
         int ys[3];
         const int ny = preimages(Y, p, H, ys);
@@ -205,32 +275,63 @@ __device__ __forceinline__ float adjoint_at(const float* __restrict__ img, int H
     return s;
 }
 
+// interior adjoint with a compile-time filter side (fully unrolled taps)
+template <int MS, bool KFLIP>
+__device__ __forceinline__ float adjoint_interior(const float* __restrict__ img, int W, int Y, int X,
+                                                  const float* __restrict__ k) {
+    constexpr int r = MS / 2;
+    const float* base = img + (size_t)(Y - r) * W + (X - r);
+    float s = 0.0f;
+#pragma unroll
+    for (int a = 0; a < MS; ++a)
+#pragma unroll
+        for (int b = 0; b < MS; ++b)
+            s = fmaf(KFLIP ? k[(MS - 1 - a) * MS + (MS - 1 - b)] : k[a * MS + b],
+                     __ldg(base + (size_t)a * W + b), s);
+    return s;
+}
+
 // v_i = conv2d_adjoint(g_t, rot180(k_i)), w1_i = phi'_i v_i
-__global__ void __launch_bounds__(256) bwd_v_kernel(const BwdArgs a) {
+template <int MS>
+__global__ void __launch_bounds__(256) bwd_v_kernel(const BwdArgs a, const PixelSet ps) {
     const int n = a.H * a.W;
-    const int i = blockIdx.x * 256 + threadIdx.x;
+    const int idx = blockIdx.x * 256 + threadIdx.x;
     const int fi = blockIdx.y;
-    if (i >= n) return;
-    const int Y = i / a.W, X = i - Y * a.W;
+    if (idx >= ps.n) return;
+    int Y, X;
+    set_pixel(ps, a.W, idx, Y, X);
+    const int i = Y * a.W + X;
     const float* k = a.s.taps + (size_t)(a.f0 + fi) * a.kp;
-    const float v = adjoint_at(a.g_t, a.H, a.W, Y, X, k, a.m, true);
+    const float v = ps.interior ? adjoint_interior<MS, true>(a.g_t, a.W, Y, X, k)
+                                : adjoint_at(a.g_t, a.H, a.W, Y, X, k, MS, true);
     const size_t o = (size_t)fi * n + i;
     a.v[o] = v;
     a.w1[o] = a.dphi[o] * v;
 }
 
-// g_prev -= conv2d_adjoint(w1_i, k_i) over the chunk's filters, ascending;
+// A_i = conv2d_adjoint(w1_i, k_i) for every (pixel, filter) of the chunk
+template <int MS>
+__global__ void __launch_bounds__(256) bwd_adj_kernel(const BwdArgs a, const PixelSet ps) {
+    const int n = a.H * a.W;
+    const int idx = blockIdx.x * 256 + threadIdx.x;
+    const int fi = blockIdx.y;
+    if (idx >= ps.n) return;
+    int Y, X;
+    set_pixel(ps, a.W, idx, Y, X);
+    const float* k = a.s.taps + (size_t)(a.f0 + fi) * a.kp;
+    const float* w1 = a.w1 + (size_t)fi * n;
+    a.adj[(size_t)fi * n + Y * a.W + X] = ps.interior ? adjoint_interior<MS, false>(w1, a.W, Y, X, k)
+                                                      : adjoint_at(w1, a.H, a.W, Y, X, k, MS, false);
+}
+
+// g_prev = ((g_t - A_0) - A_1) - ... in filter order (training.py:111-113);
 // the first chunk starts from g_t, the last adds the projected reaction term
 __global__ void __launch_bounds__(256) bwd_gprev_kernel(const BwdArgs a) {
     const int n = a.H * a.W;
     const int i = blockIdx.x * 256 + threadIdx.x;
     if (i >= n) return;
-    const int Y = i / a.W, X = i - Y * a.W;
     float g = a.f0 == 0 ? a.g_t[i] : a.g_prev[i];
-    for (int fi = 0; fi < a.nf; ++fi) {
-        const float* k = a.s.taps + (size_t)(a.f0 + fi) * a.kp;
-        g -= adjoint_at(a.w1 + (size_t)fi * n, a.H, a.W, Y, X, k, a.m, false);
-    }
+    for (int fi = 0; fi < a.nf; ++fi) g -= a.adj[(size_t)fi * n + i];
     if (a.last_chunk && a.projected) {
         const float u = a.u[i], fv = a.f[i];
         g -= a.s.lam * (-1.0f / (u * u) + 3.0f * fv * fv / (u * u * u * u)) * a.g_t[i];
@@ -238,56 +339,95 @@ __global__ void __launch_bounds__(256) bwd_gprev_kernel(const BwdArgs a) {
     a.g_prev[i] = g;
 }
 
-// per (filter, 256-pixel block) partial sums, float64, one output per thread:
-//   o <  m^2       : C1[o] = sum_P u[mir(P + off(o))] w1[P]
-//   o <  2 m^2     : C2[o - m^2] = sum_P phi[mir(P + off)] g_t[P]
-//   o <  2 m^2 + M : GW[j] = sum_P G_j(z[P]) v[P]
-// with off(a, b) = (a - r, b - r) (patch_correlation, imageops.py:109-127;
-// phi is mirror padded through mir exactly like np.pad symmetric)
-__global__ void __launch_bounds__(256) bwd_reduce_kernel(const BwdArgs a) {
+// Parameter-gradient partials of one (row y, 256-column segment, filter)
+// block, one output per warp (lanes over the segment, fixed xor-shuffle tree:
+// deterministic).  With pad = mirror padding by r (np.pad symmetric):
+//   o <  m^2       : C1[a][b] = sum_x pad(u)[y + a][x + b] w1[y][x]
+//   o <  2 m^2     : C2[a][b] = sum_x pad(phi)[y + a][x + b] g_t[y][x]
+//   o <  2 m^2 + M : GW[j]    = sum_x G_j(z[y][x]) v[y][x]
+// (patch_correlation, imageops.py:109-127; the RBF design contraction,
+// training.py:107).  The 2r+1 padded rows of u and phi, and the segment's
+// w1, g_t, z, v, are staged in shared memory.
+__device__ __forceinline__ float warp_sum(float s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+__global__ void __launch_bounds__(256) bwd_reduce_kernel(const BwdArgs a, int nseg) {
+    extern __shared__ float sm[];
     const int n = a.H * a.W;
-    const int fi = blockIdx.y, blk = blockIdx.x;
-    const int mm = a.m * a.m, nout = 2 * mm + a.s.M;
-    const int r = a.m / 2;
-    const int P0 = blk * kRedPx, P1 = min(n, P0 + kRedPx);
+    const int fi = blockIdx.y;
+    const int y = blockIdx.x / nseg, seg = blockIdx.x % nseg;
+    const int x0 = seg * kSeg, nx = min(kSeg, a.W - x0);
+    const int m = a.m, mm = m * m, r = m / 2, nout = 2 * mm + a.s.M;
+    const int SW = kSeg + 2 * r;               // staged row width
+    float* su = sm;                            // [m][SW]
+    float* sp = su + m * SW;                   // [m][SW]
+    float* sw1 = sp + m * SW;                  // [kSeg] each
+    float* sgt = sw1 + kSeg;
+    float* sz = sgt + kSeg;
+    float* sv = sz + kSeg;
     const size_t fo = (size_t)fi * n;
-    const float inv_2g2 = a.s.cE;  // -log2(e) / (2 gamma^2): G = exp2(d^2 cE)
-    for (int o = threadIdx.x; o < nout; o += blockDim.x) {
-        double acc = 0.0;
+    for (int t = threadIdx.x; t < m * SW; t += blockDim.x) {
+        const int aa = t / SW, c = t % SW;
+        const int xx = x0 + c - r;
+        float uv = 0.0f, pv = 0.0f;
+        if (c < nx + 2 * r) {
+            const size_t off = (size_t)mir1(y + aa - r, a.H) * a.W + mir1(xx, a.W);
+            uv = __ldg(a.u + off);
+            pv = __ldg(a.phi + fo + off);
+        }
+        su[t] = uv;
+        sp[t] = pv;
+    }
+    for (int t = threadIdx.x; t < kSeg; t += blockDim.x) {
+        const bool ok = t < nx;
+        const size_t off = (size_t)y * a.W + x0 + t;
+        sw1[t] = ok ? __ldg(a.w1 + fo + off) : 0.0f;
+        sgt[t] = ok ? __ldg(a.g_t + off) : 0.0f;
+        sz[t] = ok ? __ldg(a.z + fo + off) : 0.0f;
+        sv[t] = ok ? __ldg(a.v + fo + off) : 0.0f;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int o = warp; o < nout; o += nw) {
+        float s = 0.0f;
         if (o < 2 * mm) {
             const bool second = o >= mm;
             const int oo = second ? o - mm : o;
-            const int da = oo / a.m - r, db = oo % a.m - r;
-            const float* base = second ? a.phi + fo : a.u;
-            const float* adj = second ? a.g_t : a.w1 + fo;
-            float s = 0.0f;
-            for (int P = P0; P < P1; ++P) {
-                const int Y = P / a.W, X = P - Y * a.W;
-                s = fmaf(__ldg(base + (size_t)mir1(Y + da, a.H) * a.W + mir1(X + db, a.W)), __ldg(adj + P), s);
-            }
-            acc = s;
+            const float* row = (second ? sp : su) + (oo / m) * SW + (oo % m);
+            const float* adj = second ? sgt : sw1;
+            for (int x = lane; x < nx; x += 32) s = fmaf(row[x], adj[x], s);
         } else {
-            const int j = o - 2 * mm;
-            const float mu = fmaf((float)j, a.s.delta, a.s.mu0);
-            float s = 0.0f;
-            for (int P = P0; P < P1; ++P) {
-                const float d = __ldg(a.z + fo + P) - mu;
-                s = fmaf(ex2f(d * d * inv_2g2), __ldg(a.v + fo + P), s);
+            const float mu = fmaf((float)(o - 2 * mm), a.s.delta, a.s.mu0);
+            for (int x = lane; x < nx; x += 32) {
+                const float d = sz[x] - mu;
+                s = fmaf(ex2f(d * d * a.s.cE), sv[x], s);
             }
-            acc = s;
         }
-        a.part[((size_t)fi * a.nblk + blk) * nout + o] = acc;
+        s = warp_sum(s);
+        if (lane == 0) a.part[((size_t)fi * a.nblk + blockIdx.x) * nout + o] = s;
     }
 }
 
-// sum partials over blocks in block order: out[i][o] = sum_b part[i][b][o]
+// out[i][o] = sum over blocks b of part[i][b][o], one warp per output: lane
+// l sums blocks l, l + 32, ... in order, then a fixed xor tree (float64)
+__device__ __forceinline__ double warp_sum_d(double s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
 __global__ void bwd_final_kernel(const double* __restrict__ part, double* out, int nf, int nblk, int nout) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (t >= nf * nout) return;
     const int fi = t / nout, o = t - fi * nout;
     double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += part[((size_t)fi * nblk + b) * nout + o];
-    out[t] = s;
+    for (int b = lane; b < nblk; b += 32) s += part[((size_t)fi * nblk + b) * nout + o];
+    s = warp_sum_d(s);
+    if (lane == 0) out[t] = s;
 }
 
 // drop-in conv2d_adjoint (imageops.py:90-106) for one kernel
