@@ -437,7 +437,10 @@ template <int MS, bool FAST, class T>
 struct StageKernel {
     static constexpr int TH = T::TH, TW = T::TW, RB = T::RB, NT = T::NT, F = T::F;
     // m = 9 keeps 81 taps in registers: deeper forward blocking would spill
-    static constexpr int RF = MS >= 9 ? 2 : T::RF;
+#ifndef TNRD_M9_RF
+#define TNRD_M9_RF 2
+#endif
+    static constexpr int RF = MS >= 9 ? TNRD_M9_RF : T::RF;
     // 3 CTAs/SM fit the register file for m <= 7; m = 9 keeps 81 taps live
     static constexpr int MINB = T::TH == 64 ? TNRD_LARGE_MINB : (MS >= 9 ? 2 : 3);
     using C = StageCfg<MS, TH, TW, RF, RB, NT, F>;

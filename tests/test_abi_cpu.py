@@ -106,3 +106,18 @@ def test_product_package_never_imports_oracle():
                 src = open(os.path.join(root, fn)).read()
                 assert "import oracle" not in src and "from oracle" not in src, fn
                 assert "libtnrd_oracle" not in src, fn
+
+
+def test_c_example_compiles_against_the_header():
+    """examples/despeckle_c.c uses the C ABI from plain C (no Python/torch):
+    it must compile and link against include/tnrd.h + libtnrd.so."""
+    import subprocess
+    import tempfile
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "despeckle_c")
+        r = subprocess.run(["gcc", "-O2", "-Wall", "-Werror", "-I", os.path.join(repo, "include"),
+                            os.path.join(repo, "examples", "despeckle_c.c"),
+                            "-L", os.path.join(repo, "paper_1702_07482_b200"), "-ltnrd",
+                            "-lm", "-o", exe], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr

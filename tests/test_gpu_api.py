@@ -313,3 +313,22 @@ def test_projected_invalid_floor_and_smooth_max(cuda):
     assert np.abs(tn.smooth_max(x, c) - x).max() < 1e-6
     x = np.array([c - 10.0, -50.0])
     assert np.abs(tn.smooth_max(x, c) - c).max() < 1e-6
+
+
+def test_c_example_runs(cuda, tmp_path):
+    """The plain-C client of the C ABI (examples/despeckle_c.c) builds and
+    despeckles on the GPU (random model: only finiteness is checked)."""
+    import os
+    import re
+    import subprocess
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(repo, "paper_1702_07482_b200")
+    exe = str(tmp_path / "despeckle_c")
+    r = subprocess.run(["gcc", "-O2", "-I", os.path.join(repo, "include"),
+                        os.path.join(repo, "examples", "despeckle_c.c"), "-L", lib, "-ltnrd",
+                        f"-Wl,-rpath,{lib}", "-lm", "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe, "256", "320"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    m = re.search(r"checksum ([0-9.e+-]+);", r.stdout)
+    assert m and np.isfinite(float(m.group(1))) and float(m.group(1)) > 0, r.stdout
