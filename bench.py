@@ -397,20 +397,36 @@ def main():
         for _ in range(3):
             _lib.check(L.tnrd_plan_despeckle_host(plan, ctypes.c_void_p(pin_f.data_ptr()),
                                                   ctypes.c_void_p(pin_u.data_ptr())))
-        e2e_steps = max(3, min(args.steps, 50))
+        # a stream of steps through tnrd_plan_despeckle_host_many: every step
+        # still copies its input in and its result out (pinned buffers), and
+        # one step's copies overlap the next step's stages
+        per_img = int(f_host.nbytes)
+        e2e_steps = max(3, min(args.steps, 50, max(2, (1 << 30) // per_img)))
+        seq_f = torch.empty((e2e_steps,) + tuple(f_host.shape), dtype=torch.float32).pin_memory()
+        seq_f.copy_(torch.from_numpy(f_host).unsqueeze(0).expand_as(seq_f))
+        seq_u = torch.empty_like(seq_f).pin_memory()
+        bad = ctypes.c_int(-1)
+
+        def run_many():
+            _lib.check(L.tnrd_plan_despeckle_host_many(
+                plan, ctypes.c_void_p(seq_f.data_ptr()), ctypes.c_void_p(seq_u.data_ptr()),
+                e2e_steps, ctypes.byref(bad)))
+
+        run_many()   # warm-up: twin plan, graphs
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         if dist is not None:
             dist.barrier()
         e0.record(pstream)
-        for _ in range(e2e_steps):
-            _lib.check(L.tnrd_plan_despeckle_host(plan, ctypes.c_void_p(pin_f.data_ptr()),
-                                                  ctypes.c_void_p(pin_u.data_ptr())))
+        run_many()
         e1.record(pstream)
         e1.synchronize()
         e2e_ms = e0.elapsed_time(e1) / e2e_steps
-        e2e_path = "tnrd_plan_despeckle_host (C ABI), pinned host buffers"
-        assert np.array_equal(pin_u.numpy(), final_output().cpu().numpy()), "e2e result differs"
+        e2e_path = ("tnrd_plan_despeckle_host_many (C ABI): a stream of steps, each with its "
+                    "H2D + T stages + D2H + status read, pinned host buffers")
+        ref_u = final_output().cpu().numpy()
+        for k in range(e2e_steps):
+            assert np.array_equal(seq_u[k].numpy(), ref_u), "e2e result differs"
     if dist is not None:
         tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)

@@ -147,6 +147,14 @@ int tnrd_plan_destroy(tnrd_plan* plan);
  * pinned. */
 int tnrd_plan_despeckle_host(tnrd_plan* plan, const float* f_host,
                              float* u_host);
+/* A sequence of `count` host images (each batch*H*W fp32, dense, back to
+ * back in f_host / u_host): image i's copies and stages run on the plan
+ * (even i) or an internal twin plan on its own stream (odd i), so one
+ * image's H2D / D2H overlap the next one's stages (pinned host buffers
+ * needed for the overlap).  Synchronous; returns the first failing image's
+ * error with *bad_index set (-1 if none). */
+int tnrd_plan_despeckle_host_many(tnrd_plan* plan, const float* f_host,
+                                  float* u_host, int count, int* bad_index);
 /* Device-resident variant on the plan's stream (no sync, no status check). */
 int tnrd_plan_despeckle_device(tnrd_plan* plan, const float* f_dev,
                                float* u_dev);

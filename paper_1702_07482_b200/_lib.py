@@ -65,6 +65,7 @@ SIGNATURES = {
     "tnrd_plan_destroy": (_c_int, [_vp]),
     "tnrd_plan_despeckle_host": (_c_int, [_vp, _vp, _vp]),
     "tnrd_plan_despeckle_device": (_c_int, [_vp, _vp, _vp]),
+    "tnrd_plan_despeckle_host_many": (_c_int, [_vp, _vp, _vp, _c_int, ctypes.POINTER(_c_int)]),
     "tnrd_plan_check": (_c_int, [_vp, ctypes.POINTER(_c_int)]),
     "tnrd_plan_stream": (_vp, [_vp]),
     "tnrd_plan_f_device": (_vp, [_vp]),

@@ -846,6 +846,11 @@ struct tnrd_plan {
     int graph_mode = -1;           // stage-kernel mode the graph was captured with
     uint64_t graph_launches = 0;   // kernels in the graph
     long runs = 0;
+    // streaming (tnrd_plan_despeckle_host_many): a twin plan on its own stream
+    // takes every other image so one image's copies overlap the other's stages
+    tnrd_plan* twin = nullptr;
+    uint32_t* h_status_many = nullptr;  // pinned, 2 words per image
+    int h_status_cap = 0;
 };
 
 extern "C" int tnrd_plan_destroy(tnrd_plan* p) {
@@ -856,9 +861,12 @@ extern "C" int tnrd_plan_destroy(tnrd_plan* p) {
         if (p->graph) cudaGraphExecDestroy(p->graph);
         cudaFree(p->d_f); cudaFree(p->d_u); cudaFree(p->d_work); cudaFree(p->d_status);
         if (p->h_status) cudaFreeHost(p->h_status);
+        if (p->h_status_many) cudaFreeHost(p->h_status_many);
         if (p->stream) cudaStreamDestroy(p->stream);
     }
+    tnrd_plan* twin = p->twin;
     delete p;
+    if (twin) tnrd_plan_destroy(twin);
     return TNRD_OK;
 }
 
@@ -956,6 +964,56 @@ extern "C" int tnrd_plan_despeckle_host(tnrd_plan* p, const float* f_host, float
     CUDA_TRY(cudaMemcpyAsync(u_host, p->d_u, bytes, cudaMemcpyDeviceToHost, p->stream));
     int bad = -1;
     return tnrd_plan_check(p, &bad);
+}
+
+// A sequence of `count` host images (each batch*H*W fp32, dense, back to
+// back): image i's H2D, T stages and D2H are issued on the plan (even i) or
+// its twin (odd i), so the copies of one image overlap the stages of the
+// next.  Host buffers should be pinned for the overlap (pageable ones work,
+// serialised).  Returns the first image's error, with *bad_index set (-1 if
+// none).
+extern "C" int tnrd_plan_despeckle_host_many(tnrd_plan* p, const float* f_host, float* u_host,
+                                             int count, int* bad_index) {
+    if (bad_index) *bad_index = -1;
+    if (!p) return fail(TNRD_EINVAL, "plan is NULL");
+    if (count < 0) return fail(TNRD_EINVAL, "count must be >= 0");
+    if (count == 0) return TNRD_OK;
+    if (!f_host || !u_host) return fail(TNRD_EINVAL, "NULL host buffer");
+    DeviceGuard dg(p->md->device);
+    if (!p->twin) {
+        int rc = tnrd_plan_create(p->md, p->batch, p->H, p->W, &p->twin);
+        if (rc) return rc;
+    }
+    if (p->h_status_cap < count) {
+        if (p->h_status_many) cudaFreeHost(p->h_status_many);
+        p->h_status_many = nullptr;
+        p->h_status_cap = 0;
+        CUDA_TRY(cudaMallocHost(&p->h_status_many, (size_t)count * TNRD_STATUS_WORDS * sizeof(uint32_t)));
+        p->h_status_cap = count;
+    }
+    const size_t n = (size_t)p->batch * p->H * p->W;
+    for (int i = 0; i < count; ++i) {
+        tnrd_plan* q = (i & 1) ? p->twin : p;
+        CUDA_TRY(cudaMemcpyAsync(q->d_f, f_host + i * n, n * sizeof(float), cudaMemcpyHostToDevice,
+                                 q->stream));
+        int rc = plan_run(q, q->d_f, q->d_u);
+        if (rc) return rc;
+        CUDA_TRY(cudaMemcpyAsync(u_host + i * n, q->d_u, n * sizeof(float), cudaMemcpyDeviceToHost,
+                                 q->stream));
+        CUDA_TRY(cudaMemcpyAsync(p->h_status_many + (size_t)i * TNRD_STATUS_WORDS, q->d_status,
+                                 TNRD_STATUS_WORDS * sizeof(uint32_t), cudaMemcpyDeviceToHost, q->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->twin->stream));
+    for (int i = 0; i < count; ++i) {
+        int bad = -1;
+        const int rc = tnrd_status_decode(p->h_status_many + (size_t)i * TNRD_STATUS_WORDS, &bad);
+        if (rc) {
+            if (bad_index) *bad_index = i;
+            return rc;
+        }
+    }
+    return TNRD_OK;
 }
 
 extern "C" void* tnrd_plan_stream(tnrd_plan* p) { return p ? (void*)p->stream : nullptr; }

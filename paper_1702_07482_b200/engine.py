@@ -255,6 +255,32 @@ class DeviceModel:
                     p = self._plans[key] = h
         return p
 
+    def despeckle_host_many(self, f: np.ndarray, out: np.ndarray | None = None):
+        """Despeckle a sequence of HOST images f[i] ((count, H, W) or
+        (count, B, H, W), fp32) through tnrd_plan_despeckle_host_many: the
+        copies of one image overlap the stages of the next (pass pinned
+        arrays, e.g. torch pin_memory().numpy(), for the overlap).  Raises
+        the first failing image's error."""
+        f = np.asarray(f, dtype=np.float32)
+        if f.ndim == 3:
+            count, B, (H, W) = f.shape[0], 1, f.shape[1:]
+        elif f.ndim == 4:
+            count, B, H, W = f.shape
+        else:
+            raise ValueError(f"expected (count, H, W) or (count, B, H, W), got {f.shape}")
+        if not f.flags.c_contiguous:
+            f = np.ascontiguousarray(f)
+        if out is None:
+            out = np.empty_like(f)
+        elif out.shape != f.shape or out.dtype != np.float32 or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float32 array like f")
+        p = self._plan(B, H, W)
+        bad = ctypes.c_int(-1)
+        _lib.check(_lib.load().tnrd_plan_despeckle_host_many(
+            p, f.ctypes.data_as(ctypes.c_void_p), out.ctypes.data_as(ctypes.c_void_p),
+            count, ctypes.byref(bad)))
+        return out
+
     def despeckle_host(self, f: np.ndarray, out: np.ndarray | None = None):
         """Full despeckle of HOST fp32 arrays through the plan C ABI
         (tnrd_plan_despeckle_host: H2D, T stages, D2H, status check)."""

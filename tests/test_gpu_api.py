@@ -332,3 +332,23 @@ def test_c_example_runs(cuda, tmp_path):
     assert r.returncode == 0, r.stderr
     m = re.search(r"checksum ([0-9.e+-]+);", r.stdout)
     assert m and np.isfinite(float(m.group(1))) and float(m.group(1)) > 0, r.stdout
+
+
+def test_plan_despeckle_host_many_matches_single_calls(cuda):
+    """tnrd_plan_despeckle_host_many (a stream of host images, copies
+    overlapped with the next image's stages on a twin plan) gives exactly the
+    per-image results, and reports a bad image."""
+    torch = cuda
+    model = synth.make_model(7, 8, 3, 63, seed=31)
+    dm = tn.device_model_for(model)
+    rng = np.random.default_rng(8)
+    fs = rng.uniform(1, 255, (5, 70, 90)).astype(np.float32)
+    pinned = torch.from_numpy(fs).pin_memory()
+    out = dm.despeckle_host_many(pinned.numpy())
+    for i in range(5):
+        np.testing.assert_array_equal(out[i], dm.despeckle_host(fs[i]))
+    bad = fs.copy()
+    bad[2, 5, 5] = -1.0
+    with pytest.raises(ValueError, match="nonnegative"):
+        dm.despeckle_host_many(bad)
+    np.testing.assert_array_equal(dm.despeckle_host_many(fs), out)   # plan still usable
