@@ -110,7 +110,10 @@ int tnrd_model_rbf_fit(const tnrd_model* model, double* max_abs_err,
  * tile kernel with its small (32x32) / large (64x64) tiles forced, 5 = the
  * phase-locked tcgen05 kernel, 6 / 7 = CUDA-core split kernel ((tile,
  * filter group) units + ordered reduction, 2 launches per stage) with
- * large / small tiles forced.  Auto runs the split kernel on grids below
+ * large / small tiles forced, 9 = fused dataflow despeckle (all stages of
+ * tnrd_despeckle in one persistent launch, tiles of stage t+1 started as
+ * their neighbourhood of stage t is reduced; opt-in, measured slower on
+ * B200 than the per-stage split kernel).  Auto runs the split kernel on grids below
  * 3 waves of large tiles; it keeps a partial-force workspace per stream
  * inside the model (allocated on first use, outside stream capture). */
 int tnrd_set_stage_kernel(int mode);

@@ -23,6 +23,7 @@
 #include "tnrd_stage_tc.cuh"
 #include "tnrd_stage_tc3.cuh"
 #include "tnrd_speckle.cuh"
+#include "tnrd_stage_fused.cuh"
 #include "tnrd_train.cuh"
 
 using namespace tnrd;
@@ -94,20 +95,25 @@ struct tnrd_model {
     // split-kernel partial-force workspaces, one per stream (launches on one
     // stream are ordered, so a stream's workspace is never used by two
     // kernels at once); nothing in them outlives a stage
-    struct SplitBuf { void* ptr = nullptr; size_t bytes = 0; };
+    struct SplitBuf { void* ptr = nullptr; size_t bytes = 0; std::vector<long> key; };
     mutable std::mutex ws_mu;
     mutable std::map<cudaStream_t, SplitBuf> ws;
+    // fused dataflow workspaces (counters | stage args | claim sequence |
+    // partials), one per stream, rebuilt when the grid geometry changes
+    mutable std::map<cudaStream_t, SplitBuf> fws;
 };
 
 // 0 = auto (the faster kernel as measured on B200: currently
 // the CUDA-core kernels), 1 = CUDA-core only, 2 = tensor-core required,
 // 3 / 4 = CUDA-core tile kernel with small / large tiles forced (tests), 5 =
 // the phase-locked tcgen05 kernel (tnrd_stage_tc.cuh, kept for comparison),
-// 6 / 7 = CUDA-core split kernel with large / small tiles forced
+// 6 / 7 = CUDA-core split kernel with large / small tiles forced (one
+// launch pair per stage), 9 = fused dataflow despeckle (tnrd_despeckle /
+// plans: all stages in one launch; opt-in; 8 is reserved)
 static std::atomic<int> g_kernel_mode{0};
 
 extern "C" int tnrd_set_stage_kernel(int mode) {
-    if (mode < 0 || mode > 7) return fail(TNRD_EINVAL, "stage kernel mode must be in 0..7");
+    if (mode < 0 || mode > 9) return fail(TNRD_EINVAL, "stage kernel mode must be in 0..9");
     g_kernel_mode.store(mode);
     return TNRD_OK;
 }
@@ -326,6 +332,7 @@ extern "C" int tnrd_model_destroy(tnrd_model* md) {
         cudaFree(md->d_tab);
         cudaFree(md->d_bop);
         for (auto& kv : md->ws) cudaFree(kv.second.ptr);
+        for (auto& kv : md->fws) cudaFree(kv.second.ptr);
     }
     delete md;
     return TNRD_OK;
@@ -411,6 +418,98 @@ struct SplitTile { static constexpr int TH = 64, TW = 64, RF = TNRD_LARGE_RF, RB
 
 
 constexpr size_t kMaxSplitBytes = size_t(1) << 30;
+static int sm_count();
+
+// ---- fused dataflow despeckle (tnrd_stage_fused.cuh) ----------------------
+
+constexpr int kMaxFusedStages = 8;
+
+struct FusedSetup {
+    StageArgs st[kMaxFusedStages];
+    StageArgs* dst;
+    int T;
+};
+
+// stage arguments -> device memory inside the launch sequence (graph-safe:
+// no host buffer has to outlive the call)
+__global__ void fused_setup_kernel(const FusedSetup s) {
+    if ((int)threadIdx.x < s.T) s.dst[threadIdx.x] = s.st[threadIdx.x];
+}
+
+struct FusedLayout {
+    size_t ctl, stargs, seq, part0, part1, bytes;
+    int nclaims;
+};
+
+static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+// claim sequence: (stage, tile, group pair) ordered by tile + D * stage, with
+// D = one tile row + 1 (the dependency reach) + one wave of claims
+#ifndef TNRD_FUSED_CLAIM
+#define TNRD_FUSED_CLAIM 2
+#endif
+constexpr int kFusedClaim = TNRD_FUSED_CLAIM;   // filter groups per claim
+
+static std::vector<int> fused_sequence(int T, int tiles, int tiles_x, int ng, int grid) {
+    const int pairs = (ng + kFusedClaim - 1) / kFusedClaim;
+    const int lag = (grid + pairs - 1) / pairs;
+    const int D = tiles_x + 1 + lag;
+    std::vector<int> seq;
+    seq.reserve((size_t)T * tiles * pairs);
+    for (long w = 0; w < (long)D * (T - 1) + tiles; ++w)
+        for (int t = 0; t < T; ++t) {
+            const long tile = w - (long)D * t;
+            if (tile < 0 || tile >= tiles) continue;
+            for (int pr = 0; pr < pairs; ++pr) seq.push_back((t << 24) | ((int)tile << 6) | (kFusedClaim * pr));
+        }
+    return seq;
+}
+
+static FusedLayout fused_layout(int T, int tiles, int ng, int tpx, int nclaims) {
+    FusedLayout L;
+    L.ctl = 0;
+    L.stargs = align256(sizeof(uint32_t) * (2 + 2 * (size_t)T * tiles));
+    L.seq = L.stargs + align256(sizeof(StageArgs) * T);
+    L.part0 = L.seq + align256(sizeof(int) * (size_t)nclaims);
+    const size_t part = align256(sizeof(float) * (size_t)tiles * ng * tpx);
+    L.part1 = L.part0 + part;
+    L.bytes = L.part1 + part;
+    L.nclaims = nclaims;
+    return L;
+}
+
+// the stream's fused workspace for this geometry: (re)built outside capture
+static int fused_workspace(const tnrd_model* md, cudaStream_t s, const std::vector<long>& key,
+                           int T, int tiles, int tiles_x, int ng, int tpx, int grid, void** out,
+                           FusedLayout* lay) {
+    std::lock_guard<std::mutex> lk(md->ws_mu);
+    auto& b = md->fws[s];
+    if (b.key != key) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+        if (cs != cudaStreamCaptureStatusNone)
+            return fail(TNRD_ECUDA, "fused workspace must be built before stream capture");
+        const std::vector<int> seq = fused_sequence(T, tiles, tiles_x, ng, grid);
+        const FusedLayout L = fused_layout(T, tiles, ng, tpx, (int)seq.size());
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (b.ptr) cudaFree(b.ptr);
+        b.ptr = nullptr;
+        b.bytes = 0;
+        b.key.clear();
+        CUDA_TRY(cudaMalloc(&b.ptr, L.bytes));
+        CUDA_TRY(cudaMemset(b.ptr, 0, L.stargs));   // cursor, counters, flags
+        CUDA_TRY(cudaMemcpy(static_cast<char*>(b.ptr) + L.seq, seq.data(), seq.size() * sizeof(int),
+                            cudaMemcpyHostToDevice));
+        b.bytes = L.bytes;
+        b.key = key;
+    }
+    const int pairs = (ng + kFusedClaim - 1) / kFusedClaim;
+    *lay = fused_layout(T, tiles, ng, tpx, T * tiles * pairs);
+    *out = b.ptr;
+    return TNRD_OK;
+}
+
+
 
 // Launch with programmatic stream serialization: the kernel may be scheduled
 // while its predecessor on the stream drains, and waits for it with
@@ -469,6 +568,67 @@ struct StageKernel {
         b.ngroups = (a.nk + F - 1) / F;
         CUDA_TRY(launch_pdl(kern, dim3((a.W + TW - 1) / TW, (a.H + TH - 1) / TH, batch), NT, smem, s, b));
         g_launches.fetch_add(1);
+        return TNRD_OK;
+    }
+
+    // all T stages in one persistent dataflow launch (+ the setup kernel)
+    static int launch_fused(const tnrd_model* md, const StageArgs* st, int nst, int batch,
+                            cudaStream_t s) {
+        const int T_ = nst;
+        static std::mutex mu;
+        static uint64_t attr_set = 0;
+        static int occ[64] = {0};
+        const size_t smem = C::smem_bytes(st[0].tab_stride);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        auto kern = fused::despeckle_fused_kernel<MS, TH, TW, RF, RB, NT, FAST, F, MINB>;
+        int rc = prepare(kern, dev, attr_set, mu);
+        if (rc) return rc;
+        int per_sm = 0;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            per_sm = occ[dev & 63];
+            if (per_sm == 0) {
+                CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+                occ[dev & 63] = per_sm = std::max(per_sm, 1);
+            }
+        }
+        const int ng = (st[0].nk + F - 1) / F;
+        const int tiles_x = (st[0].W + TW - 1) / TW, tiles_y = (st[0].H + TH - 1) / TH;
+        const int tiles = tiles_x * tiles_y * batch;
+        const int grid = std::min(sm_count() * per_sm, T_ * tiles * ((ng + kFusedClaim - 1) / kFusedClaim));
+        const std::vector<long> key = {tiles_x, tiles_y, tiles, T_, ng, grid, MS, TH};
+        void* wsp = nullptr;
+        FusedLayout L;
+        rc = fused_workspace(md, s, key, T_, tiles, tiles_x, ng, TH * TW, grid, &wsp, &L);
+        if (rc) return rc;
+        char* base = static_cast<char*>(wsp);
+        FusedSetup su;
+        su.T = T_;
+        su.dst = reinterpret_cast<StageArgs*>(base + L.stargs);
+        for (int t = 0; t < T_; ++t) {
+            su.st[t] = st[t];
+            su.st[t].ngroups = ng;
+        }
+        fused_setup_kernel<<<1, 32, 0, s>>>(su);
+        CUDA_TRY(cudaGetLastError());
+        fused::FusedArgs fa;
+        fa.st = su.dst;
+        fa.seq = reinterpret_cast<const int*>(base + L.seq);
+        fa.nclaims = L.nclaims;
+        fa.T = T_;
+        fa.claim_groups = kFusedClaim;
+        fa.part0 = reinterpret_cast<float*>(base + L.part0);
+        fa.part1 = reinterpret_cast<float*>(base + L.part1);
+        fa.ctl = reinterpret_cast<uint32_t*>(base + L.ctl);
+        fa.cnt = fa.ctl + 2;
+        fa.done = fa.cnt + (size_t)T_ * tiles;
+        fa.tiles_x = tiles_x;
+        fa.tiles_y = tiles_y;
+        fa.tiles = tiles;
+        kern<<<grid, NT, smem, s>>>(fa);
+        CUDA_TRY(cudaGetLastError());
+        g_launches.fetch_add(2);
         return TNRD_OK;
     }
 
@@ -810,6 +970,45 @@ extern "C" int tnrd_stage(const tnrd_model* md, int t, const float* u_in, const 
                         (cudaStream_t)stream);
 }
 
+// One fused dataflow launch for all T stages (mode 9).  Returns -1 when not
+// applicable.
+template <bool FAST>
+static int despeckle_fused_m(const tnrd_model* md, const StageArgs* st, int batch, cudaStream_t s) {
+    switch (md->m) {
+        case 3: return StageKernel<3, FAST, SplitTile>::launch_fused(md, st, md->T, batch, s);
+        case 5: return StageKernel<5, FAST, SplitTile>::launch_fused(md, st, md->T, batch, s);
+        case 7: return StageKernel<7, FAST, SplitTile>::launch_fused(md, st, md->T, batch, s);
+        default: return StageKernel<9, FAST, SplitTile>::launch_fused(md, st, md->T, batch, s);
+    }
+}
+
+static int despeckle_fused(const tnrd_model* md, const float* f, float* u_out, float* work, int batch,
+                           int H, int W, int64_t ld, int64_t image_stride, uint32_t* d_status,
+                           cudaStream_t s) {
+    // opt-in (mode 9): measured slower than the per-stage split kernel on
+    // C2, kept for the dataflow experiments
+    const int mode = g_kernel_mode.load();
+    if (mode != 9) return -1;
+    if (md->T > kMaxFusedStages || md->T < 1) return -1;
+    StageArgs st[kMaxFusedStages];
+    const float* cur = f;
+    for (int t = 0; t < md->T; ++t) {
+        float* dst = ((md->T - 1 - t) % 2 == 0) ? u_out : work;
+        const uint32_t fl = t == 0 ? (TNRD_STAGE_FLOOR_INPUT | TNRD_STAGE_CHECK_F) : 0u;
+        st[t] = stage_args(md, t, fl);
+        st[t].u_in = cur; st[t].f = f; st[t].u_out = dst;
+        st[t].ld = ld; st[t].img_stride = image_stride;
+        st[t].H = H; st[t].W = W;
+        st[t].status = d_status;
+        cur = dst;
+    }
+    const int ng = (md->nk + SplitTile::F - 1) / SplitTile::F;
+    const long tiles = StageKernel<7, true, SplitTile>::tiles(st[0], batch);
+    if (ng > 63 || tiles >= (1l << 18)) return -1;
+    if ((size_t)tiles * ng * SplitTile::TH * SplitTile::TW * sizeof(float) * 2 > kMaxSplitBytes) return -1;
+    return md->fast ? despeckle_fused_m<true>(md, st, batch, s) : despeckle_fused_m<false>(md, st, batch, s);
+}
+
 extern "C" int tnrd_despeckle(const tnrd_model* md, const float* f, float* u_out, float* work,
                               int batch, int H, int W, int64_t ld, int64_t image_stride,
                               uint32_t* d_status, void* stream) {
@@ -820,6 +1019,8 @@ extern "C" int tnrd_despeckle(const tnrd_model* md, const float* f, float* u_out
     if (rc) return rc;
     DeviceGuard dg(md->device);
     cudaStream_t s = (cudaStream_t)stream;
+    rc = despeckle_fused(md, f, u_out, work, batch, H, W, ld, image_stride, d_status, s);
+    if (rc != -1) return rc;   // ran (or failed) as one fused launch
     const float* cur = f;
     for (int t = 0; t < md->T; ++t) {
         float* dst = ((md->T - 1 - t) % 2 == 0) ? u_out : work;
@@ -1019,6 +1220,14 @@ extern "C" int tnrd_plan_despeckle_host_many(tnrd_plan* p, const float* f_host, 
 extern "C" void* tnrd_plan_stream(tnrd_plan* p) { return p ? (void*)p->stream : nullptr; }
 extern "C" float* tnrd_plan_f_device(tnrd_plan* p) { return p ? p->d_f : nullptr; }
 extern "C" float* tnrd_plan_u_device(tnrd_plan* p) { return p ? p->d_u : nullptr; }
+
+#ifdef TNRD_FUSED_TRACE
+extern "C" __attribute__((visibility("default"))) int tnrd_debug_fused_trace(long long* out, int n) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpyFromSymbol(out, fused::g_fused_trace, (size_t)std::min(n, 4096) * 5 * sizeof(long long)));
+    return TNRD_OK;
+}
+#endif
 
 #ifdef TNRD_SPLIT_TRACE
 extern "C" __attribute__((visibility("default"))) int tnrd_debug_split_trace(unsigned long long* out, int n) {

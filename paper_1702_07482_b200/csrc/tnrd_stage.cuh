@@ -223,7 +223,9 @@ struct StageCfg {
 // u tile with a 2r halo, mirrored at image edges (or read from the halo rows
 // of a row strip), floored on the first stage (initial_state,
 // diffusion.py:219-224)
-template <class C, int NT>
+// COHERENT: u was written earlier in the same kernel (the fused dataflow
+// kernel) -- read through L2 (ld.global.cg), not the read-only path
+template <class C, int NT, bool COHERENT = false>
 __device__ __forceinline__ void stage_u_tile(const StageArgs& p, float* sU, const float* __restrict__ uin,
                                              int Y0, int X0, bool top_halo, bool bot_halo, int tid) {
     constexpr int R = C::R;
@@ -240,7 +242,7 @@ __device__ __forceinline__ void stage_u_tile(const StageArgs& p, float* sU, cons
                 const int X = mirror_clamp(X0 - 2 * R + ux, p.W);
                 if (Y < 0) Y = top_halo ? max(Y, -2 * R) : mirror_clamp(Y, p.H);
                 else if (Y >= p.H) Y = bot_halo ? min(Y, p.H - 1 + 2 * R) : mirror_clamp(Y, p.H);
-                v[j] = __ldg(uin + (int64_t)Y * p.ld + X);
+                v[j] = COHERENT ? __ldcg(uin + (int64_t)Y * p.ld + X) : __ldg(uin + (int64_t)Y * p.ld + X);
             }
         }
 #pragma unroll

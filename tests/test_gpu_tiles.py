@@ -119,3 +119,30 @@ def test_auto_small_grid_uses_split_and_matches_tile_kernel(cuda):
         _lib.set_stage_kernel(_lib.KERNEL_AUTO)
     a, b = a.cpu().numpy(), b.cpu().numpy()
     assert np.max(np.abs(a - b) / b) < 1e-5
+
+
+@pytest.mark.parametrize("shape", [(512, 512), (1, 300, 200), (3, 130, 250), (97, 333)])
+def test_fused_dataflow_bit_identical_to_split_stages(cuda, shape):
+    """The fused dataflow despeckle (all stages in one launch, tiles of stage
+    t+1 started as their neighbourhood of stage t is reduced) sums the same
+    partials in the same order as the per-stage split kernel: bit-identical
+    output, including the projected variant."""
+    torch = cuda
+    for variant in ("prox", "projected"):
+        model = synth.make_model(7, 12, 4, 63, seed=len(shape) * 10 + shape[-1])
+        model.variant = variant
+        dm = tn.device_model_for(model)
+        f = torch.from_numpy(np.random.default_rng(1).uniform(1, 255, shape).astype(np.float32)).cuda()
+        _lib.set_stage_kernel(9)
+        try:
+            _lib.launch_count_reset()
+            fused = dm.despeckle(f)
+            torch.cuda.synchronize()
+            assert _lib.launch_count() == 2          # setup + one dataflow kernel
+            fused2 = dm.despeckle(f)
+            _lib.set_stage_kernel(_lib.KERNEL_SPLIT_LARGE)
+            split = dm.despeckle(f)
+        finally:
+            _lib.set_stage_kernel(_lib.KERNEL_AUTO)
+        assert torch.equal(fused, split)
+        assert torch.equal(fused, fused2)
