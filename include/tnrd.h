@@ -110,13 +110,19 @@ int tnrd_model_rbf_fit(const tnrd_model* model, double* max_abs_err,
  * tile kernel with its small (32x32) / large (64x64) tiles forced, 5 = the
  * phase-locked tcgen05 kernel, 6 / 7 = CUDA-core split kernel ((tile,
  * filter group) units + ordered reduction, 2 launches per stage) with
- * large / small tiles forced, 9 = fused dataflow despeckle (all stages of
+ * large / small tiles forced, 8 = z-field stage (tcgen05 forward filter
+ * bank over the whole image into per-stream z planes, then a TMA-fed
+ * CUDA-core RBF + adjoint + prox kernel; m <= 7, nk <= 128), 9 = fused dataflow despeckle (all stages of
  * tnrd_despeckle in one persistent launch, tiles of stage t+1 started as
  * their neighbourhood of stage t is reduced; opt-in, measured slower on
  * B200 than the per-stage split kernel).  Auto runs the split kernel on grids below
  * 3 waves of large tiles; it keeps a partial-force workspace per stream
  * inside the model (allocated on first use, outside stream capture). */
 int tnrd_set_stage_kernel(int mode);
+/* z-field stage precision (process-wide): number of tf32 cross products of
+ * the 3-piece splits of u and k -- 6 (default: below fp32 rounding), 4 or 3
+ * (experiments). */
+int tnrd_set_zfield_passes(int n);
 
 /* Reset a device status block (stream-ordered memset). */
 int tnrd_status_reset(uint32_t* d_status, void* stream);

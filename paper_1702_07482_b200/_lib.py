@@ -53,6 +53,7 @@ SIGNATURES = {
                                     ctypes.POINTER(_c_dbl),
                                     ctypes.POINTER(_c_int)]),
     "tnrd_set_stage_kernel": (_c_int, [_c_int]),
+    "tnrd_set_zfield_passes": (_c_int, [_c_int]),
     "tnrd_status_reset": (_c_int, [_vp, _vp]),
     "tnrd_status_decode": (_c_int, [ctypes.POINTER(_c_u32),
                                     ctypes.POINTER(_c_int)]),
@@ -113,6 +114,9 @@ def load():
         mode = os.environ.get("TNRD_STAGE_KERNEL")  # experiments: 0 auto, 1 cuda-core, 2 tcgen05
         if mode:
             L.tnrd_set_stage_kernel(int(mode))
+        passes = os.environ.get("TNRD_ZF_PASSES")  # experiments: 3, 4 or 6
+        if passes:
+            L.tnrd_set_zfield_passes(int(passes))
     return _lib
 
 
@@ -143,6 +147,7 @@ KERNEL_AUTO, KERNEL_CUDA_CORE, KERNEL_TENSOR_CORE = 0, 1, 2
 KERNEL_SMALL_TILES, KERNEL_LARGE_TILES = 3, 4
 KERNEL_TC_PHASED = 5
 KERNEL_SPLIT_LARGE, KERNEL_SPLIT_SMALL = 6, 7
+KERNEL_ZFIELD = 8
 
 
 def set_stage_kernel(mode: int) -> None:

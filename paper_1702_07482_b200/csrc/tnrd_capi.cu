@@ -6,12 +6,14 @@
 // the caller exactly as diffusion.py:76-77 does; this file only casts them
 // and builds the RBF tables), then everything is uploaded once per model.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <type_traits>
@@ -22,6 +24,7 @@
 #include "tnrd_stage.cuh"
 #include "tnrd_stage_tc.cuh"
 #include "tnrd_stage_tc3.cuh"
+#include "tnrd_stage_zf.cuh"
 #include "tnrd_speckle.cuh"
 #include "tnrd_stage_fused.cuh"
 #include "tnrd_train.cuh"
@@ -92,6 +95,10 @@ struct tnrd_model {
     // [nk_pad/16 groups][m][ksteps][2 prec][2 kc][16][4]
     float* d_bop = nullptr;
     size_t bop_stage = 0;     // floats per stage
+    // z-field forward operand (tnrd_stage_zf.cuh, m <= 7, nk_pad <= 128): per
+    // stage [m][ksteps][3 pieces][2 kc][nk_pad][4] of kf = rot180(k)
+    float* d_zop = nullptr;
+    size_t zop_stage = 0;
     // split-kernel partial-force workspaces, one per stream (launches on one
     // stream are ordered, so a stream's workspace is never used by two
     // kernels at once); nothing in them outlives a stage
@@ -101,6 +108,8 @@ struct tnrd_model {
     // fused dataflow workspaces (counters | stage args | claim sequence |
     // partials), one per stream, rebuilt when the grid geometry changes
     mutable std::map<cudaStream_t, SplitBuf> fws;
+    // z-field planes (tnrd_stage_zf.cuh), one per stream
+    mutable std::map<cudaStream_t, SplitBuf> zws;
 };
 
 // 0 = auto (the faster kernel as measured on B200: currently
@@ -109,7 +118,8 @@ struct tnrd_model {
 // the phase-locked tcgen05 kernel (tnrd_stage_tc.cuh, kept for comparison),
 // 6 / 7 = CUDA-core split kernel with large / small tiles forced (one
 // launch pair per stage), 9 = fused dataflow despeckle (tnrd_despeckle /
-// plans: all stages in one launch; opt-in; 8 is reserved)
+// plans: all stages in one launch; opt-in), 8 = z-field stage
+// (tnrd_stage_zf.cuh: tcgen05 forward over the image + TMA-fed RBF/adjoint)
 static std::atomic<int> g_kernel_mode{0};
 
 extern "C" int tnrd_set_stage_kernel(int mode) {
@@ -291,14 +301,52 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
                                     bop[base + bo + (kc * tc::kG + n) * 4 + e] = tf32_rna_host(v - hi);
                                 }
     }
+    // z-field forward operand: kf = rot180(k) split into 3 tf32 pieces
+    // (hi, mid, lo), K-major [kc][n][4] per (tap row a, K-step, piece)
+    std::vector<float> zop;
+    if (m <= 7 && md->nk_pad <= 128) {
+        const int ks = (m + 7) / 8, np = md->nk_pad;
+        const size_t bo = 2 * (size_t)np * 4;
+        md->zop_stage = (size_t)m * ks * zf::kPieces * bo;
+        zop.assign(md->zop_stage * T, 0.0f);
+        for (int t = 0; t < T; ++t)
+            for (int a = 0; a < m; ++a)
+                for (int kk = 0; kk < ks; ++kk)
+                    for (int kc = 0; kc < 2; ++kc)
+                        for (int n = 0; n < np; ++n)
+                            for (int e = 0; e < 4; ++e) {
+                                const int b = 8 * kk + 4 * kc + e;
+                                float v = 0.0f;
+                                if (n < nk && b < m)
+                                    v = (float)kernels[(((size_t)t * nk + n) * m + (m - 1 - a)) * m + (m - 1 - b)];
+                                float r = v;
+                                for (int pc = 0; pc < zf::kPieces; ++pc) {
+                                    const float h = tf32_rna_host(r);
+                                    r = r - h;
+                                    zop[(size_t)t * md->zop_stage + ((size_t)(a * ks + kk) * zf::kPieces + pc) * bo +
+                                        ((size_t)kc * np + n) * 4 + e] = h;
+                                }
+                            }
+    }
     {
         DeviceGuard dg(device);
+        if (!zop.empty()) {
+            cudaError_t ez = cudaMalloc(&md->d_zop, zop.size() * sizeof(float));
+            if (ez == cudaSuccess)
+                ez = cudaMemcpy(md->d_zop, zop.data(), zop.size() * sizeof(float), cudaMemcpyHostToDevice);
+            if (ez != cudaSuccess) {
+                cudaFree(md->d_zop);
+                delete md;
+                return fail(TNRD_ECUDA, "z-field operand upload failed: %s", cudaGetErrorString(ez));
+            }
+        }
         if (!bop.empty()) {
             cudaError_t eb = cudaMalloc(&md->d_bop, bop.size() * sizeof(float));
             if (eb == cudaSuccess)
                 eb = cudaMemcpy(md->d_bop, bop.data(), bop.size() * sizeof(float), cudaMemcpyHostToDevice);
             if (eb != cudaSuccess) {
                 cudaFree(md->d_bop);
+                cudaFree(md->d_zop);
                 delete md;
                 return fail(TNRD_ECUDA, "tensor-core operand upload failed: %s", cudaGetErrorString(eb));
             }
@@ -306,7 +354,7 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
         cudaError_t e1 = cudaMalloc(&md->d_taps, ntap * sizeof(float));
         cudaError_t e2 = cudaMalloc(&md->d_tab, ntab * sizeof(float));
         if (e1 != cudaSuccess || e2 != cudaSuccess) {
-            cudaFree(md->d_taps); cudaFree(md->d_tab); cudaFree(md->d_bop);
+            cudaFree(md->d_taps); cudaFree(md->d_tab); cudaFree(md->d_bop); cudaFree(md->d_zop);
             delete md;
             return fail(TNRD_ECUDA, "cudaMalloc of model parameters failed: %s",
                         cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
@@ -314,7 +362,7 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
         cudaError_t e3 = cudaMemcpy(md->d_taps, taps.data(), ntap * sizeof(float), cudaMemcpyHostToDevice);
         cudaError_t e4 = cudaMemcpy(md->d_tab, tab.data(), ntab * sizeof(float), cudaMemcpyHostToDevice);
         if (e3 != cudaSuccess || e4 != cudaSuccess) {
-            cudaFree(md->d_taps); cudaFree(md->d_tab); cudaFree(md->d_bop);
+            cudaFree(md->d_taps); cudaFree(md->d_tab); cudaFree(md->d_bop); cudaFree(md->d_zop);
             delete md;
             return fail(TNRD_ECUDA, "parameter upload failed: %s",
                         cudaGetErrorString(e3 != cudaSuccess ? e3 : e4));
@@ -331,7 +379,9 @@ extern "C" int tnrd_model_destroy(tnrd_model* md) {
         cudaFree(md->d_taps);
         cudaFree(md->d_tab);
         cudaFree(md->d_bop);
+        cudaFree(md->d_zop);
         for (auto& kv : md->ws) cudaFree(kv.second.ptr);
+        for (auto& kv : md->zws) cudaFree(kv.second.ptr);
         for (auto& kv : md->fws) cudaFree(kv.second.ptr);
     }
     delete md;
@@ -891,6 +941,208 @@ static int dispatch_tc(const tnrd_model* md, int t, StageArgs a, int batch, cuda
 }
 
 
+// ---- z-field stage (tnrd_stage_zf.cuh): tcgen05 forward -> z planes, then
+// TMA-fed RBF + adjoint + prox ------------------------------------------------
+
+#ifndef TNRD_ZF_PASSES
+#define TNRD_ZF_PASSES 6
+#endif
+static std::atomic<int> g_zf_passes{TNRD_ZF_PASSES};
+
+extern "C" int tnrd_set_zfield_passes(int n) {
+    if (n != 3 && n != 4 && n != 6) return fail(TNRD_EINVAL, "z-field pass count must be 3, 4 or 6");
+    g_zf_passes.store(n);
+    return TNRD_OK;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static std::atomic<PFN_cuTensorMapEncodeTiled_v12000> fn{nullptr};
+    PFN_cuTensorMapEncodeTiled_v12000 f = fn.load();
+    if (!f) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            f = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+        fn.store(f);
+    }
+    return f;
+}
+
+// z-stage tile configurations: large tiles for batches / big scenes, small
+// tiles (half height) when the grid would not fill the SMs; both keep one
+// filter split (NSPLIT = 1), so the per-pixel summation order -- and the
+// result bits -- do not depend on the choice
+struct ZTileL { static constexpr int TH = 64, TW = 64, RB = 4, NT = 256, F = 2, MINB = 2; };
+struct ZTileS { static constexpr int TH = 32, TW = 64, RB = 2, NT = 256, F = 2, MINB = 2; };
+
+template <int MS, int NP>
+static int launch_zfield(const zf::ZArgs& z, int gx, int gy, int batch, cudaStream_t s) {
+    using C = zf::ZCfg<MS, NP>;
+    static std::mutex mu;
+    static uint64_t attr_set = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto kern = zf::zfield_kernel<MS, NP>;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!(attr_set & (1ull << (dev & 63)))) {
+            CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)C::smem_bytes()));
+            attr_set |= 1ull << (dev & 63);
+        }
+    }
+    CUDA_TRY(launch_pdl(kern, dim3(gx, gy, batch), zf::kZThreads, C::smem_bytes(), s, z));
+    return TNRD_OK;
+}
+
+template <int MS, class T>
+static int launch_zstage(const zf::ZStageArgs& za, const CUtensorMap& map, int batch, cudaStream_t s) {
+    using C = zf::ZSCfg<MS, T::TH, T::TW, T::RB, T::NT, T::F>;
+    static std::mutex mu;
+    static uint64_t attr_set = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto kern = zf::zstage_kernel<MS, T::TH, T::TW, T::RB, T::NT, T::F, T::MINB>;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!(attr_set & (1ull << (dev & 63)))) {
+            CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr_set |= 1ull << (dev & 63);
+        }
+    }
+    const size_t smem = C::smem_bytes(za.s.tab_stride);
+    dim3 grid((za.s.W + T::TW - 1) / T::TW, (za.s.H + T::TH - 1) / T::TH, batch);
+    CUDA_TRY(launch_pdl(kern, grid, T::NT, smem, s, za, map));
+    return TNRD_OK;
+}
+
+template <int MS>
+static int dispatch_zfield_np(int np, const zf::ZArgs& z, int gx, int gy, int batch, cudaStream_t s) {
+    switch (np) {
+        case 16: return launch_zfield<MS, 16>(z, gx, gy, batch, s);
+        case 32: return launch_zfield<MS, 32>(z, gx, gy, batch, s);
+        case 48: return launch_zfield<MS, 48>(z, gx, gy, batch, s);
+        case 64: return launch_zfield<MS, 64>(z, gx, gy, batch, s);
+        case 80: return launch_zfield<MS, 80>(z, gx, gy, batch, s);
+        case 96: return launch_zfield<MS, 96>(z, gx, gy, batch, s);
+        case 112: return launch_zfield<MS, 112>(z, gx, gy, batch, s);
+        case 128: return launch_zfield<MS, 128>(z, gx, gy, batch, s);
+        default: return fail(TNRD_EUNSUPPORTED, "z-field kernel: nk_pad %d", np);
+    }
+}
+
+template <class T>
+static int dispatch_zstage_m(int m, const zf::ZStageArgs& za, const CUtensorMap& map, int batch,
+                             cudaStream_t s) {
+    switch (m) {
+        case 3: return launch_zstage<3, T>(za, map, batch, s);
+        case 5: return launch_zstage<5, T>(za, map, batch, s);
+        case 7: return launch_zstage<7, T>(za, map, batch, s);
+        default: return fail(TNRD_EUNSUPPORTED, "z-field stage: m=%d", m);
+    }
+}
+
+static bool zf_supported(const tnrd_model* md) {
+    return md->fast && md->d_zop && md->m <= 7 && md->nk_pad <= 128 && tensor_map_encoder() != nullptr;
+}
+
+static int launch_zf(const tnrd_model* md, int t, const StageArgs& a, int batch, cudaStream_t s) {
+    const int m = md->m, R = m / 2, np = md->nk_pad;
+    const bool top_halo = a.flags & TNRD_STAGE_TOP_HALO, bot_halo = a.flags & TNRD_STAGE_BOTTOM_HALO;
+    const int64_t zld = round_up(a.W + 2 * R, 4);   // plane column = image column + r
+    const int64_t zrows = a.H + 2 * R;
+    const int64_t zplane = zrows * zld;
+    const size_t bytes = (size_t)batch * np * zplane * sizeof(float);
+    // the stream's z planes, grown on demand (outside capture)
+    float* zbuf = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(md->ws_mu);
+        auto& b = md->zws[s];
+        if (b.bytes < bytes) {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+            if (cs != cudaStreamCaptureStatusNone)
+                return fail(TNRD_ECUDA, "z-field workspace must be allocated before stream capture");
+            if (b.ptr) {
+                CUDA_TRY(cudaStreamSynchronize(s));
+                cudaFree(b.ptr);
+                b.ptr = nullptr;
+                b.bytes = 0;
+            }
+            CUDA_TRY(cudaMalloc(&b.ptr, bytes));
+            b.bytes = bytes;
+        }
+        zbuf = static_cast<float*>(b.ptr);
+    }
+    zf::ZArgs z;
+    z.u_in = a.u_in; z.ld = a.ld; z.img_stride = a.img_stride;
+    z.H = a.H; z.W = a.W;
+    z.flags = a.flags & (TNRD_STAGE_FLOOR_INPUT | TNRD_STAGE_TOP_HALO | TNRD_STAGE_BOTTOM_HALO);
+    z.u0_floor = a.u0_floor;
+    z.bop = md->d_zop + (size_t)t * md->zop_stage;
+    z.z = zbuf; z.zld = zld; z.zplane = zplane; z.zimg = np * zplane;
+    z.zrow0 = top_halo ? -R : 0;
+    z.zrow_end = bot_halo ? a.H + R : a.H;
+    const int np_ = g_zf_passes.load();
+    // (u piece, k piece) products, largest first
+    static const int pu6[6] = {0, 1, 0, 2, 1, 0}, pk6[6] = {0, 0, 1, 0, 1, 2};
+    static const int pu4[4] = {0, 1, 0, 1}, pk4[4] = {0, 0, 1, 1};
+    const int* pu = np_ == 4 ? pu4 : pu6;
+    const int* pk = np_ == 4 ? pk4 : pk6;
+    z.npass = np_;
+    z.pass_u = 0; z.pass_k = 0;
+    for (int i = 0; i < np_; ++i) {
+        z.pass_u |= (uint32_t)pu[i] << (2 * i);
+        z.pass_k |= (uint32_t)pk[i] << (2 * i);
+    }
+    const int gx = (a.W + R + zf::kBandCols - 1) / zf::kBandCols;   // bands start at 32 bx - r
+    const int gy = (z.zrow_end - z.zrow0 + zf::kBandRows - 1) / zf::kBandRows;
+    int rc = TNRD_OK;
+    switch (m) {
+        case 3: rc = dispatch_zfield_np<3>(np, z, gx, gy, batch, s); break;
+        case 5: rc = dispatch_zfield_np<5>(np, z, gx, gy, batch, s); break;
+        case 7: rc = dispatch_zfield_np<7>(np, z, gx, gy, batch, s); break;
+        default: return fail(TNRD_EUNSUPPORTED, "z-field kernel: m=%d", m);
+    }
+    if (rc) return rc;
+    static const int zf_debug = getenv("TNRD_ZF_DEBUG") ? atoi(getenv("TNRD_ZF_DEBUG")) : 0;
+    if (zf_debug == 1) return TNRD_OK;   // zfield only
+    if (zf_debug == 2) {
+        CUDA_TRY(cudaStreamSynchronize(s));
+        fprintf(stderr, "zf debug: zfield ok\n");
+    }
+
+    const bool large = (long)((a.W + 63) / 64) * ((a.H + 63) / 64) * batch >= 2L * sm_count();
+    const int F = large ? ZTileL::F : ZTileS::F;
+    const int TH = large ? ZTileL::TH : ZTileS::TH, TW = large ? ZTileL::TW : ZTileS::TW;
+    CUtensorMap map;
+    {
+        const cuuint64_t dims[3] = {(cuuint64_t)zld, (cuuint64_t)zrows, (cuuint64_t)batch * np};
+        const cuuint64_t strides[2] = {(cuuint64_t)zld * 4, (cuuint64_t)zplane * 4};
+        const cuuint32_t box[3] = {(cuuint32_t)round_up(TW + 2 * R, 4), (cuuint32_t)(TH + 2 * R), (cuuint32_t)F};
+        const cuuint32_t es[3] = {1, 1, 1};
+        CUresult r = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, zbuf, dims, strides, box, es,
+                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(TNRD_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
+    zf::ZStageArgs za;
+    za.s = a;
+    za.s.ngroups = (md->nk + F - 1) / F;
+    za.np = np;
+    rc = large ? dispatch_zstage_m<ZTileL>(m, za, map, batch, s) : dispatch_zstage_m<ZTileS>(m, za, map, batch, s);
+    if (rc) return rc;
+    if (zf_debug == 2) {
+        CUDA_TRY(cudaStreamSynchronize(s));
+        fprintf(stderr, "zf debug: zstage ok\n");
+    }
+    g_launches.fetch_add(2);
+    return TNRD_OK;
+}
+
+
 static int check_shape(const tnrd_model* md, int batch, int H, int W, int64_t ld,
                        int64_t image_stride) {
     if (batch < 1 || batch > 65535) return fail(TNRD_EINVAL, "batch must be in [1, 65535], got %d", batch);
@@ -951,7 +1203,8 @@ static int launch_stage(const tnrd_model* md, int t, const float* u_in, const fl
     const int mode = g_kernel_mode.load();
     if (mode == 2 && tc3_supported(md)) return dispatch_tc3(md, t, a, batch, s);
     if (mode == 5 && tc_supported(md)) return dispatch_tc(md, t, a, batch, s);
-    if (mode == 2 || mode == 5)
+    if (mode == 8 && zf_supported(md)) return launch_zf(md, t, a, batch, s);
+    if (mode == 2 || mode == 5 || mode == 8)
         return fail(TNRD_EUNSUPPORTED, "tensor-core stage kernel unavailable for this model");
     return md->fast ? dispatch_m<true>(md, a, batch, s) : dispatch_m<false>(md, a, batch, s);
 }
