@@ -412,7 +412,7 @@ def main():
                 plan, ctypes.c_void_p(seq_f.data_ptr()), ctypes.c_void_p(seq_u.data_ptr()),
                 e2e_steps, ctypes.byref(bad)))
 
-        run_many()   # warm-up: twin plan, graphs
+        run_many()   # warm-up: twin plans, graphs
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         if dist is not None:

@@ -336,7 +336,7 @@ def test_c_example_runs(cuda, tmp_path):
 
 def test_plan_despeckle_host_many_matches_single_calls(cuda):
     """tnrd_plan_despeckle_host_many (a stream of host images, copies
-    overlapped with the next image's stages on a twin plan) gives exactly the
+    overlapped with the next images' stages on chained twin plans) gives exactly the
     per-image results, and reports a bad image."""
     torch = cuda
     model = synth.make_model(7, 8, 3, 63, seed=31)
