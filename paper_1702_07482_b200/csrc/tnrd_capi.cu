@@ -82,7 +82,7 @@ struct tnrd_model {
     double mu0 = 0, delta = 0, gamma = 0;
     double zlo = 0, h = 0;  // polynomial intervals: centre j at zlo + j h
     int ni = 0;             // number of intervals
-    int nip = 0;            // intervals rounded to 4 (coefficient-plane stride)
+    int nip = 0;            // intervals rounded to 8 (whole 8-interval table blocks)
     double fit_err = 0;     // max |p(z) - phi(z)| over all filters/stages
     double fit_err32 = 0;   // same with the fp32 coefficients
     double fit_scale = 0;   // max sum_j |w_ij|
@@ -160,7 +160,7 @@ static double phi_exact(const double* w, int M, double mu0, double delta, double
 // check points and, in *err32, the same with the fp32-rounded coefficients
 // the kernel uses.
 static double fit_interval(const double* w, int M, double mu0, double delta, double gamma,
-                           double zc, double h, float* out, int swap, double* err32) {
+                           double zc, double h, float* out, double* err32) {
     constexpr int N = kPolyDeg + 1;
     long double A[N][N + 1];
     for (int k = 0; k < N; ++k) {
@@ -186,7 +186,7 @@ static double fit_interval(const double* w, int M, double mu0, double delta, dou
     for (int d = 0; d < N; ++d) {
         c[d] = (double)(A[d][N] / A[d][d]);
         c32[d] = (float)c[d];
-        out[swap ? (d ^ 4) : d] = c32[d];  // float4 halves swapped (bank spread)
+        out[(d >> 2) * 32 + (d & 3)] = c32[d];   // c0..c3 | c4..c7 at +32 floats (rbf_lo_offset)
     }
     double err = 0.0, e32 = 0.0;
     for (int k = 0; k <= 40; ++k) {
@@ -244,7 +244,7 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
     md->zlo = mu0 - 7.0 * gamma;
     const double zhi = mu0 + (M - 1) * delta + 7.0 * gamma;
     md->ni = (int)std::ceil((zhi - md->zlo) / md->h) + 1;
-    md->nip = md->ni;
+    md->nip = round_up(md->ni, 8);   // whole 8-interval blocks (rbf_lo_offset)
     md->fast = (size_t)md->nip * kPolyN * kF <= 16384;  // <= 64 KB per group buffer
     md->tab_stride = md->fast ? md->nip * kPolyN : round_up(M, 4);
 
@@ -267,7 +267,7 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
                     md->fit_err = std::max(md->fit_err,
                                            fit_interval(w, M, mu0, delta, gamma,
                                                         md->zlo + q * md->h, md->h,
-                                                        tb + (size_t)q * kPolyN, (q >> 2) & 1, &e32));
+                                                        tb + rbf_lo_offset(q), &e32));
                     md->fit_err32 = std::max(md->fit_err32, e32);
                 }
             } else {
@@ -1173,6 +1173,7 @@ static StageArgs stage_args(const tnrd_model* md, int t, uint32_t flags) {
     a.inv2a = (float)(1.0 / (2.0 * aa));
     const double L2E = 1.4426950408889634;
     a.inv_h = (float)(1.0 / md->h);
+    a.tab_bias = 0u - (0x4B400000u << 5);
     a.tab_ni = md->nip;
     a.t_off = (float)(-md->zlo / md->h);
     a.tmax = (float)(md->ni - 1);

@@ -74,6 +74,7 @@ struct StageArgs {
     // RBF: polynomial table (default) -- t = z / h + t_off, clamp [0, tmax];
     // interval j at tab[8 j], halves swapped when bit 2 of j is set
     float inv_h;
+    uint32_t tab_bias;   // -(0x4B400000 << 5) mod 2^32, a runtime value so ptxas keeps it in the table base register
     int tab_ni;
     float t_off;
     float tmax;
@@ -152,23 +153,15 @@ __device__ __forceinline__ int mirror_clamp(int j, int n) {
 //   float64 at 8 Chebyshev nodes of every interval of width
 //   h = min(delta, gamma) / 2 covering [mu_0 - 7 gamma, mu_{M-1} + 7 gamma]
 //   and stores the degree-7 interpolant's monomial coefficients in the local
-//   variable x in [-1/2, 1/2]: interval j holds 8 floats, the two float4
-//   halves swapped when bit 2 of j is set, so that the 16-byte loads of 8
-//   lanes whose intervals are consecutive hit 8 distinct bank quads.
-//   Interpolation error ~1e-9 * sum|w| (checked on the host at model
-//   creation); no MUFU, 2 LDS.128 + 7 FFMA per response
-//   instead of 63 exp + 63 FMA.
-__device__ __forceinline__ float rbf_poly(float z, const float* __restrict__ tabf,
-                                          const StageArgs& p) {
-    float t = fmaf(z, p.inv_h, p.t_off);
-    t = fminf(fmaxf(t, 0.0f), p.tmax);
-    const float r = t + 12582912.0f;                 // rint(t) in the low bits
-    const int j = __float_as_int(r) - 0x4B400000;
-    const float x = t - (r - 12582912.0f);           // in [-1/2, 1/2]
-    const int sw = (j >> 2) & 1;
-    const float* c = tabf + j * kPolyN;
-    const float4 lo = *reinterpret_cast<const float4*>(c + 4 * sw);        // c0..c3
-    const float4 hi = *reinterpret_cast<const float4*>(c + 4 * (sw ^ 1));  // c4..c7
+//   variable x in [-1/2, 1/2].  Layout: blocks of 8 intervals, 64 floats
+//   each -- c0..c3 of the 8 intervals, then c4..c7 -- so 8 lanes reading 8
+//   consecutive intervals hit 8 distinct bank quads and the second half is
+//   an immediate +128 B.  Interpolation error ~1e-9 * sum|w| (checked on the
+//   host at model creation); no MUFU, 2 LDS.128 + 7 FFMA
+//   per response instead of 63 exp + 63 FMA.
+__host__ __device__ constexpr int rbf_lo_offset(int j) { return (j >> 3) * 64 + (j & 7) * 4; }
+
+__device__ __forceinline__ float rbf_horner(float x, float4 lo, float4 hi) {
     float acc = fmaf(hi.w, x, hi.z);
     acc = fmaf(acc, x, hi.y);
     acc = fmaf(acc, x, hi.x);
@@ -176,6 +169,43 @@ __device__ __forceinline__ float rbf_poly(float z, const float* __restrict__ tab
     acc = fmaf(acc, x, lo.z);
     acc = fmaf(acc, x, lo.y);
     return fmaf(acc, x, lo.x);
+}
+
+// generic-pointer version (tables in global or shared memory)
+__device__ __forceinline__ float rbf_poly(float z, const float* __restrict__ tabf,
+                                          const StageArgs& p) {
+    float t = fmaf(z, p.inv_h, p.t_off);
+    t = fminf(fmaxf(t, 0.0f), p.tmax);
+    const float r = t + 12582912.0f;                 // rint(t) in the low bits
+    const int j = __float_as_int(r) - 0x4B400000;
+    const float x = t - (r - 12582912.0f);           // in [-1/2, 1/2]
+    const float* c = tabf + rbf_lo_offset(j);
+    return rbf_horner(x, *reinterpret_cast<const float4*>(c), *reinterpret_cast<const float4*>(c + 32));
+}
+
+// shared-memory version for the stage kernels: `tb` = the table's shared
+// address + p.tab_bias (= -(0x4B400000 << 5), a runtime value so ptxas keeps
+// it folded in the register); with b = the rounded float's bits, interval
+// j = b - 0x4B400000 starts at tb + (b >> 3) * 128 + b * 16 (3 integer
+// instructions, both halves at immediate offsets)
+__device__ __forceinline__ uint32_t rbf_table_base(const float* tabf, const StageArgs& p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(tabf)) + p.tab_bias;
+}
+
+__device__ __forceinline__ float rbf_poly_s(float z, uint32_t tb, const StageArgs& p) {
+    float t = fmaf(z, p.inv_h, p.t_off);
+    t = fminf(fmaxf(t, 0.0f), p.tmax);
+    const float r = t + 12582912.0f;
+    const float x = t - (r - 12582912.0f);
+    const uint32_t b = static_cast<uint32_t>(__float_as_int(r));
+    const uint32_t a = ((b >> 3) << 7) + (b << 4) + tb;
+    float4 lo, hi;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%8];\n\t"
+                 "ld.shared.v4.f32 {%4, %5, %6, %7}, [%8+128];"
+                 : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+                 : "r"(a)
+                 : "memory");
+    return rbf_horner(x, lo, hi);
 }
 
 // phi(z) as the reference writes it: all M centres (generic bandwidths).
@@ -289,6 +319,7 @@ __device__ __forceinline__ void forward_group(const StageArgs& p, const float* s
     float k[C::KK];
     load_taps<C>(tapg + fi * C::KP, k);
     const float* tabf = tabg + fi * p.tab_stride;
+    const uint32_t tb = rbf_table_base(tabf, p);
     float* phif = sPhi + fi * C::SPHI;
     for (int blk = tid - fi * C::TPF; blk < C::NBLK; blk += C::TPF) {
         const int by = blk / C::NBX;
@@ -327,10 +358,10 @@ __device__ __forceinline__ void forward_group(const StageArgs& p, const float* s
         for (int r = 0; r < RF; ++r) {
             float4 o;
             if (FAST) {
-                o.x = rbf_poly(acc[r][0], tabf, p);
-                o.y = rbf_poly(acc[r][1], tabf, p);
-                o.z = rbf_poly(acc[r][2], tabf, p);
-                o.w = rbf_poly(acc[r][3], tabf, p);
+                o.x = rbf_poly_s(acc[r][0], tb, p);
+                o.y = rbf_poly_s(acc[r][1], tb, p);
+                o.z = rbf_poly_s(acc[r][2], tb, p);
+                o.w = rbf_poly_s(acc[r][3], tb, p);
             } else {
                 o.x = rbf_direct(acc[r][0], tabf, p);
                 o.y = rbf_direct(acc[r][1], tabf, p);

@@ -366,12 +366,12 @@ __global__ void __launch_bounds__(NT, MINB) zstage_kernel(const ZStageArgs za,
         constexpr int Q = C::SPHI / 4;
         for (int i = tid; i < F * Q; i += NT) {
             const int fi = i / Q;
-            const float* tabf = tabg + fi * p.tab_stride;
+            const uint32_t tb = rbf_table_base(tabg + fi * p.tab_stride, p);
             float4 z = *reinterpret_cast<const float4*>(ph + 4 * i);
-            z.x = rbf_poly(z.x, tabf, p);
-            z.y = rbf_poly(z.y, tabf, p);
-            z.z = rbf_poly(z.z, tabf, p);
-            z.w = rbf_poly(z.w, tabf, p);
+            z.x = rbf_poly_s(z.x, tb, p);
+            z.y = rbf_poly_s(z.y, tb, p);
+            z.z = rbf_poly_s(z.z, tb, p);
+            z.w = rbf_poly_s(z.w, tb, p);
             *reinterpret_cast<float4*>(ph + 4 * i) = z;
         }
         __syncthreads();

@@ -51,10 +51,9 @@ __device__ __forceinline__ float rbf_poly_deriv(float z, const float* __restrict
     const float r = t + 12582912.0f;
     const int j = __float_as_int(r) - 0x4B400000;
     const float x = t - (r - 12582912.0f);
-    const int sw = (j >> 2) & 1;
-    const float* c = tabf + j * kPolyN;
-    const float4 lo = *reinterpret_cast<const float4*>(c + 4 * sw);
-    const float4 hi = *reinterpret_cast<const float4*>(c + 4 * (sw ^ 1));
+    const float* c = tabf + rbf_lo_offset(j);
+    const float4 lo = *reinterpret_cast<const float4*>(c);
+    const float4 hi = *reinterpret_cast<const float4*>(c + 32);
     float acc = fmaf(7.0f * hi.w, x, 6.0f * hi.z);
     acc = fmaf(acc, x, 5.0f * hi.y);
     acc = fmaf(acc, x, 4.0f * hi.x);
