@@ -1306,6 +1306,13 @@ struct tnrd_plan {
     tnrd_plan* twin = nullptr;
     uint32_t* h_status_many = nullptr;  // pinned, 2 words per image
     int h_status_cap = 0;
+    // banded host path for one large scene (plan_banded_host): row bands on
+    // their own streams, H2D / D2H streams, per-band events
+    int nbands = 0;
+    std::vector<cudaStream_t> band_streams;
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_stage;  // [band], [2][band]
+    cudaEvent_t ev_reset = nullptr;
 };
 
 extern "C" int tnrd_plan_destroy(tnrd_plan* p) {
@@ -1317,6 +1324,12 @@ extern "C" int tnrd_plan_destroy(tnrd_plan* p) {
         cudaFree(p->d_f); cudaFree(p->d_u); cudaFree(p->d_work); cudaFree(p->d_status);
         if (p->h_status) cudaFreeHost(p->h_status);
         if (p->h_status_many) cudaFreeHost(p->h_status_many);
+        for (cudaStream_t bs : p->band_streams) { cudaStreamSynchronize(bs); cudaStreamDestroy(bs); }
+        if (p->copy_in) { cudaStreamSynchronize(p->copy_in); cudaStreamDestroy(p->copy_in); }
+        if (p->copy_out) { cudaStreamSynchronize(p->copy_out); cudaStreamDestroy(p->copy_out); }
+        for (cudaEvent_t e : p->ev_in) cudaEventDestroy(e);
+        for (cudaEvent_t e : p->ev_stage) cudaEventDestroy(e);
+        if (p->ev_reset) cudaEventDestroy(p->ev_reset);
         if (p->stream) cudaStreamDestroy(p->stream);
     }
     tnrd_plan* twin = p->twin;
@@ -1408,10 +1421,114 @@ extern "C" int tnrd_plan_check(tnrd_plan* p, int* bad_stage) {
     return tnrd_status_decode(p->h_status, bad_stage);
 }
 
+// Row bands for one large scene: band boundaries on multiples of the large
+// tile height (the band launches then see the same tile grid as the whole
+// image, so the result is bit-identical), every band >= 3 waves of large
+// tiles (the tile kernel, as for the whole image), at most 16 bands.
+// 0 = do not band (small images, batches, CUDA-core kernels not in auto mode).
+static int band_count(const tnrd_model* md, int batch, int H, int W) {
+    static const int env = [] {
+        const char* e = getenv("TNRD_SCENE_BANDS");
+        return e ? std::min(std::max(atoi(e), 1), 64) : 0;
+    }();
+    if (batch != 1 || g_kernel_mode.load() != 0) return 0;
+    const long tiles_x = (W + LargeTile::TW - 1) / LargeTile::TW;
+    const long row_tiles = (H + LargeTile::TH - 1) / LargeTile::TH;
+    const long wave3 = 3L * 2 * sm_count();
+    long nb = env ? env : std::min<long>(16, (row_tiles * tiles_x) / wave3);
+    nb = std::min(nb, row_tiles);
+    return nb >= 2 ? (int)nb : 0;
+}
+
+static int banded_setup(tnrd_plan* p, int nb) {
+    if (p->nbands == nb) return TNRD_OK;
+    for (cudaStream_t bs : p->band_streams) { cudaStreamSynchronize(bs); cudaStreamDestroy(bs); }
+    for (cudaEvent_t e : p->ev_in) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->ev_stage) cudaEventDestroy(e);
+    p->band_streams.clear(); p->ev_in.clear(); p->ev_stage.clear();
+    p->nbands = 0;
+    if (!p->copy_in) CUDA_TRY(cudaStreamCreateWithFlags(&p->copy_in, cudaStreamNonBlocking));
+    if (!p->copy_out) CUDA_TRY(cudaStreamCreateWithFlags(&p->copy_out, cudaStreamNonBlocking));
+    if (!p->ev_reset) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_reset, cudaEventDisableTiming));
+    p->band_streams.resize(nb);
+    p->ev_in.resize(nb);
+    p->ev_stage.resize(2 * (size_t)nb);
+    for (int b = 0; b < nb; ++b) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&p->band_streams[b], cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_in[b], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_stage[b], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&p->ev_stage[nb + b], cudaEventDisableTiming));
+    }
+    p->nbands = nb;
+    return TNRD_OK;
+}
+
+// One large scene from/to HOST memory with the copies overlapped: the scene
+// is cut into nb row bands; band b's H2D, its T stage launches (row-strip
+// halo mode: the neighbouring bands' rows are read in place) and its D2H
+// run on their own streams, ordered by events only where the data flows --
+// stage t of band b after stage t-1 of bands b-1, b, b+1 (its halo rows;
+// also the write-after-read of the ping-pong buffer), stage 0 after the
+// H2D of bands b-1..b+1, the D2H of band b after its last stage.  So the
+// first stages start after 2/nb of the input has landed and the last
+// bands' output copies overlap the remaining stages.
+static int plan_banded_host(tnrd_plan* p, const float* f_host, float* u_host, int nb) {
+    const tnrd_model* md = p->md;
+    int rc = banded_setup(p, nb);
+    if (rc) return rc;
+    const int H = p->H, W = p->W, T = md->T;
+    const int row_tiles = (H + LargeTile::TH - 1) / LargeTile::TH;
+    std::vector<int> r0(nb + 1);
+    for (int b = 0; b <= nb; ++b) r0[b] = std::min(H, (int)((long)row_tiles * b / nb) * LargeTile::TH);
+    rc = tnrd_status_reset(p->d_status, p->copy_in);
+    if (rc) return rc;
+    for (int b = 0; b < nb; ++b) {
+        const size_t off = (size_t)r0[b] * W, n = (size_t)(r0[b + 1] - r0[b]) * W;
+        CUDA_TRY(cudaMemcpyAsync(p->d_f + off, f_host + off, n * sizeof(float), cudaMemcpyHostToDevice,
+                                 p->copy_in));
+        CUDA_TRY(cudaEventRecord(p->ev_in[b], p->copy_in));
+    }
+    for (int t = 0; t < T; ++t) {
+        const float* src = t == 0 ? p->d_f : (((T - t) % 2 == 0) ? p->d_u : p->d_work);
+        float* dst = ((T - 1 - t) % 2 == 0) ? p->d_u : p->d_work;
+        cudaEvent_t* prev = p->ev_stage.data() + (size_t)((t + 1) % 2) * nb;
+        cudaEvent_t* cur = p->ev_stage.data() + (size_t)(t % 2) * nb;
+        for (int b = 0; b < nb; ++b) {
+            cudaStream_t s = p->band_streams[b];
+            for (int nbh = std::max(0, b - 1); nbh <= std::min(nb - 1, b + 1); ++nbh) {
+                if (t == 0) CUDA_TRY(cudaStreamWaitEvent(s, p->ev_in[nbh], 0));
+                else if (nbh != b) CUDA_TRY(cudaStreamWaitEvent(s, prev[nbh], 0));
+            }
+            uint32_t fl = t == 0 ? (TNRD_STAGE_FLOOR_INPUT | TNRD_STAGE_CHECK_F) : 0u;
+            if (b > 0) fl |= TNRD_STAGE_TOP_HALO;
+            if (b + 1 < nb) fl |= TNRD_STAGE_BOTTOM_HALO;
+            const size_t off = (size_t)r0[b] * W;
+            rc = launch_stage(md, t, src + off, p->d_f + off, dst + off, 1, r0[b + 1] - r0[b], W, W,
+                              (int64_t)W * H, fl, p->d_status, s);
+            if (rc) return rc;
+            CUDA_TRY(cudaEventRecord(cur[b], s));
+        }
+    }
+    cudaEvent_t* last = p->ev_stage.data() + (size_t)((T - 1) % 2) * nb;
+    for (int b = 0; b < nb; ++b) {
+        const size_t off = (size_t)r0[b] * W, n = (size_t)(r0[b + 1] - r0[b]) * W;
+        CUDA_TRY(cudaStreamWaitEvent(p->copy_out, last[b], 0));
+        CUDA_TRY(cudaMemcpyAsync(u_host + off, p->d_u + off, n * sizeof(float), cudaMemcpyDeviceToHost,
+                                 p->copy_out));
+    }
+    CUDA_TRY(cudaMemcpyAsync(p->h_status, p->d_status, TNRD_STATUS_WORDS * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, p->copy_out));
+    CUDA_TRY(cudaStreamSynchronize(p->copy_out));
+    int bad = -1;
+    return tnrd_status_decode(p->h_status, &bad);
+}
+
 extern "C" int tnrd_plan_despeckle_host(tnrd_plan* p, const float* f_host, float* u_host) {
     if (!p) return fail(TNRD_EINVAL, "plan is NULL");
     if (!f_host || !u_host) return fail(TNRD_EINVAL, "NULL host buffer");
     DeviceGuard dg(p->md->device);
+    const int nb = band_count(p->md, p->batch, p->H, p->W);
+    if (nb >= 2) return plan_banded_host(p, f_host, u_host, nb);
     const size_t bytes = (size_t)p->batch * p->H * p->W * sizeof(float);
     CUDA_TRY(cudaMemcpyAsync(p->d_f, f_host, bytes, cudaMemcpyHostToDevice, p->stream));
     int rc = plan_run(p, p->d_f, p->d_u);
