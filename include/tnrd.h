@@ -153,7 +153,12 @@ int tnrd_plan_create(const tnrd_model* model, int batch, int H, int W,
 int tnrd_plan_destroy(tnrd_plan* plan);
 /* Full despeckle from/to HOST buffers (batch*H*W fp32, dense): H2D, all T
  * stages, D2H, synchronise, decode status.  Host buffers may be pageable or
- * pinned. */
+ * pinned.  A single image of >= 2 x 3 waves of 64x64 tiles (e.g. a 16384^2
+ * scene) runs as up to 16 tile-aligned row bands on their own streams, each
+ * band's H2D, T stages (neighbour rows read in place) and D2H ordered by
+ * events only where data flows, so the copies overlap the stages (pinned
+ * buffers needed for the overlap; TNRD_SCENE_BANDS overrides the count).
+ * The result is bit-identical to the unbanded despeckle. */
 int tnrd_plan_despeckle_host(tnrd_plan* plan, const float* f_host,
                              float* u_host);
 /* A sequence of `count` host images (each batch*H*W fp32, dense, back to
