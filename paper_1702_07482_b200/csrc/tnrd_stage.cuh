@@ -259,7 +259,8 @@ template <class C, int NT, bool COHERENT = false>
 __device__ __forceinline__ void stage_u_tile(const StageArgs& p, float* sU, const float* __restrict__ uin,
                                              int Y0, int X0, bool top_halo, bool bot_halo, int tid) {
     constexpr int R = C::R;
-    constexpr int B = 8;  // loads in flight per thread
+    // all of the tile's loads in flight at once (one L2 round trip, not three)
+    constexpr int B = (C::SU + NT - 1) / NT < 32 ? (C::SU + NT - 1) / NT : 32;
     const bool floor_in = p.flags & 0x1u;
     for (int i0 = tid; i0 < C::SU; i0 += B * NT) {
         float v[B];
