@@ -9,7 +9,10 @@ key = sys.argv[1] if len(sys.argv) > 1 else "c3"
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 cfg = synth.CONFIGS[key]
 model = synth.config_model(cfg)
-f = torch.from_numpy(np.stack([synth.noisy_image(cfg, i)[1] for i in range(B)])).cuda()
+if cfg.tiled:
+    f = torch.from_numpy(np.ascontiguousarray(synth.scene_crop(cfg, 0, cfg.H, 0, cfg.W), dtype=np.float32)).cuda()
+else:
+    f = torch.from_numpy(np.stack([synth.noisy_image(cfg, i)[1] for i in range(B)])).cuda()
 dm = tn.device_model_for(model)
 for _ in range(3):
     dm.despeckle(f)

@@ -1,0 +1,24 @@
+#!/bin/bash
+# One round's measurement set on a GPU box (run under gpurun): bench lines of
+# every workload + the reference arm, the ncu launch list of the default
+# bench command, and ncu --set full captures of the top kernels.
+# Usage: bash tools/round_profile.sh <outdir under gpurun_out/>
+set -u
+O=gpurun_out/$1
+mkdir -p $O
+python bench.py > $O/bench_c2.json 2> $O/bench_c2.err
+python bench.py --workload c3 --steps 10 --warmup 3 > $O/bench_c3.json 2> $O/bench_c3.err
+python bench.py --workload c4 --steps 5 --warmup 3 > $O/bench_c4.json 2> $O/bench_c4.err
+python bench.py --workload c5 --steps 10 --warmup 3 > $O/bench_c5.json 2> $O/bench_c5.err
+python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c2.csv \
+    python bench.py --steps 20 --warmup 3 --no-cpu-baseline > $O/ncu_launch.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:stage_kernel_split -s 10 -c 1 \
+    -o $O/c2_split python tools/prof_one.py c2 1 > $O/ncu_c2.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:stage_reduce -s 10 -c 1 \
+    -o $O/c2_reduce python tools/prof_one.py c2 1 > $O/ncu_c2r.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:stage_kernel -s 2 -c 1 \
+    -o $O/c3_tile python tools/prof_one.py c3 256 > $O/ncu_c3.log 2>&1
+ncu --set full --clock-control none -k regex:stage_kernel -s 2 -c 1 \
+    -o $O/c4_tile python tools/prof_one.py c4 1 > $O/ncu_c4.log 2>&1
+ls -la $O
