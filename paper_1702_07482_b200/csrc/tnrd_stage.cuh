@@ -312,7 +312,7 @@ __device__ __forceinline__ void load_taps(const float* tap, float (&k)[C::KK]) {
 
 // forward: z = conv(u, k) on the phi region, phi = rbf(z); TPF threads per
 // filter, each with the filter's taps in registers
-template <class C, int MS, int RF, int F, bool FAST, bool BATCH_RBF = true>
+template <class C, int MS, int RF, int F, bool FAST, int BATCH_ROWS = RF>
 __device__ __forceinline__ void forward_group(const StageArgs& p, const float* sU, float* sPhi,
                                               const float* tapg, const float* tabg, int tid) {
     constexpr int R = C::R;
@@ -355,11 +355,11 @@ __device__ __forceinline__ void forward_group(const StageArgs& p, const float* s
             }
         }
         float* dst = phif + y0 * C::PW + x0;
-        // BATCH_RBF: all RF x 4 table lookups before the first phi store
+        // BATCH_ROWS = RF: all RF x 4 table lookups before the first phi store
         // (the lookups are ordered asm loads with a memory clobber, so a
         // store between rows caps the lookups in flight at one row's four).
         // Measured on B200: +5% for the tile kernel (C3), -7% for the split
-        // kernel (C2), which therefore keeps the per-row stores.
+        // kernel (C2), which therefore stores in smaller row batches.
         float4 o[RF];
 #pragma unroll
         for (int r = 0; r < RF; ++r) {
@@ -374,11 +374,12 @@ __device__ __forceinline__ void forward_group(const StageArgs& p, const float* s
                 o[r].z = rbf_direct(acc[r][2], tabf, p);
                 o[r].w = rbf_direct(acc[r][3], tabf, p);
             }
-            if (!BATCH_RBF) *reinterpret_cast<float4*>(dst + r * C::PW) = o[r];
-        }
-        if (BATCH_RBF) {
+            // store rows in batches of BATCH_ROWS (all RF rows: one batch)
+            if ((r + 1) % BATCH_ROWS == 0 || r == RF - 1) {
 #pragma unroll
-            for (int r = 0; r < RF; ++r) *reinterpret_cast<float4*>(dst + r * C::PW) = o[r];
+                for (int q = r - (r % BATCH_ROWS); q <= r; ++q)
+                    *reinterpret_cast<float4*>(dst + q * C::PW) = o[q];
+            }
         }
     }
 }
@@ -623,6 +624,9 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const StageArgs p) {
 // The summation order is fixed by the unit structure, not by which CTA ran
 // what, so results are bit-reproducible and identical for any grid (strips
 // == whole image).  No state survives a launch.
+#ifndef TNRD_SPLIT_RBF_ROWS
+#define TNRD_SPLIT_RBF_ROWS 1   // phi rows per store batch in the split kernel's forward
+#endif
 struct SplitWs {
     float* part;       // [tiles][ngroups][TH*TW] partial forces
     int tiles_x, tiles_y, tiles;
@@ -686,7 +690,7 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel_split(const StageArgs p
         if (unit + 1 < uend) prefetch_group<C, F, NT>(p, sTap, sTab, (unit + 1) % ng, buf ^ 1, tid);
         const float* tapg = sTap + buf * F * C::KP;
         const float* tabg = sTab + buf * tabsz;
-        forward_group<C, MS, RF, F, FAST, false>(p, sU, sPhi, tapg, tabg, tid);
+        forward_group<C, MS, RF, F, FAST, TNRD_SPLIT_RBF_ROWS>(p, sU, sPhi, tapg, tabg, tid);
         __syncthreads();
         fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
         float force[RB][4];
