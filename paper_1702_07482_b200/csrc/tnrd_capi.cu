@@ -90,6 +90,7 @@ struct tnrd_model {
     int variant = 0;          // 0 prox, 1 projected (tnrd_model_set_variant)
     double floor = 1.0;       // projection floor
     float* d_taps = nullptr;  // T * nk_pad * kp
+    std::vector<float> h_taps;  // host copy (parameter-space taps, TapBlock)
     float* d_tab = nullptr;   // T * nk_pad * tab_stride
     // tensor-core forward GEMM operand (m in {3,5,7}): per stage
     // [nk_pad/16 groups][m][ksteps][2 prec][2 kc][16][4]
@@ -359,6 +360,7 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
             return fail(TNRD_ECUDA, "cudaMalloc of model parameters failed: %s",
                         cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
         }
+        md->h_taps.assign(taps.begin(), taps.begin() + ntap);
         cudaError_t e3 = cudaMemcpy(md->d_taps, taps.data(), ntap * sizeof(float), cudaMemcpyHostToDevice);
         cudaError_t e4 = cudaMemcpy(md->d_tab, tab.data(), ntab * sizeof(float), cudaMemcpyHostToDevice);
         if (e3 != cudaSuccess || e4 != cudaSuccess) {
@@ -448,6 +450,32 @@ extern "C" int tnrd_status_decode(const uint32_t* h, int* bad_stage) {
 // from the sweeps in DESIGN.md §5: small tiles keep a single 512^2 image
 // spread over all 148 SMs; large tiles cut the phi-halo recompute
 // (inflation 1.48 -> 1.23) once the grid has enough tiles.
+// parameter-space taps kernels (stage_kernel_pt / stage_kernel_split_pt):
+// forward blocking and CTAs per SM (the taps no longer hold registers)
+#ifndef TNRD_PT_RF
+#define TNRD_PT_RF 5
+#endif
+#ifndef TNRD_PT_MINB
+#define TNRD_PT_MINB 2
+#endif
+// tile kernel with parameter-space taps: filters per group and CTAs per SM
+// (the split kernel keeps SplitTile's groups: they size its workspace)
+#ifndef TNRD_PT_TILE_F
+#define TNRD_PT_TILE_F 2
+#endif
+#ifndef TNRD_PT_TILE_MINB
+#define TNRD_PT_TILE_MINB 2
+#endif
+// TNRD_PARAM_TAPS=0 in the environment selects the shared-memory-taps
+// kernels (A/B measurements)
+static bool param_taps_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TNRD_PARAM_TAPS");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 struct SmallTile { static constexpr int TH = 32, TW = 32, RF = 2, RB = 2, NT = 256, F = 4; };
 #ifndef TNRD_LARGE_RF
 #define TNRD_LARGE_RF 5
@@ -605,18 +633,52 @@ struct StageKernel {
         return TNRD_OK;
     }
 
-    static int launch(const StageArgs& a, int batch, cudaStream_t s) {
+    // parameter-space taps (TapBlock, tnrd_stage.cuh): large tiles only (one
+    // thread per output block, so the tap address is warp-uniform)
+    // (m <= 7: 81 taps of m = 9 exceed the 63 uniform registers per warp --
+    // measured 19% slower on C5)
+    static constexpr bool kPT = T::TH == 64 && FAST && MS <= 7;
+    using TB = TapBlock<2560>;
+    static constexpr int RF_PT = TNRD_PT_RF;
+    static constexpr int F_TILE_PT = TNRD_PT_TILE_F;
+    using CP = StageCfg<MS, TH, TW, RF_PT, RB, NT, F>;
+    using CPT = StageCfg<MS, TH, TW, RF_PT, RB, NT, F_TILE_PT>;
+    // htaps: this stage's taps on the host, [nk_pad][kp]
+    static bool pt_fits(const StageArgs& a) {
+        return kPT && param_taps_enabled() &&
+               (size_t)round_up(a.nk, 4) * C::KP <= sizeof(TB) / sizeof(float);
+    }
+    static void fill_taps(TB& tb, const float* htaps, int nk) {
+        std::memcpy(tb.k, htaps, sizeof(float) * (size_t)round_up(nk, 4) * C::KP);
+    }
+
+    static int launch(const StageArgs& a, int batch, cudaStream_t s, const float* htaps = nullptr) {
         static std::mutex mu;
         static uint64_t attr_set = 0;  // per-device bitmask
-        const size_t smem = C::smem_bytes(a.tab_stride);
         int dev = 0;
         cudaGetDevice(&dev);
+        StageArgs b = a;
+        b.ngroups = (a.nk + F - 1) / F;
+        const dim3 grid((a.W + TW - 1) / TW, (a.H + TH - 1) / TH, batch);
+        if constexpr (kPT) {
+            if (htaps && pt_fits(a)) {
+                static std::mutex mu2;
+                static uint64_t attr2 = 0;
+                auto kern = stage_kernel_pt<MS, TH, TW, RF_PT, RB, NT, FAST, F_TILE_PT, TNRD_PT_TILE_MINB, TB>;
+                int rc = prepare(kern, dev, attr2, mu2);
+                if (rc) return rc;
+                TB tb;
+                fill_taps(tb, htaps, a.nk);
+                b.ngroups = (a.nk + F_TILE_PT - 1) / F_TILE_PT;
+                CUDA_TRY(launch_pdl(kern, grid, NT, CPT::smem_bytes(a.tab_stride), s, b, tb));
+                g_launches.fetch_add(1);
+                return TNRD_OK;
+            }
+        }
         auto kern = stage_kernel<MS, TH, TW, RF, RB, NT, FAST, F, MINB>;
         int rc = prepare(kern, dev, attr_set, mu);
         if (rc) return rc;
-        StageArgs b = a;
-        b.ngroups = (a.nk + F - 1) / F;
-        CUDA_TRY(launch_pdl(kern, dim3((a.W + TW - 1) / TW, (a.H + TH - 1) / TH, batch), NT, smem, s, b));
+        CUDA_TRY(launch_pdl(kern, grid, NT, C::smem_bytes(a.tab_stride), s, b));
         g_launches.fetch_add(1);
         return TNRD_OK;
     }
@@ -691,14 +753,33 @@ struct StageKernel {
     }
 
     // persistent grid of (SMs x resident CTAs) over (tile, group) units
-    static int launch_split(const StageArgs& a, int batch, void* wsp, cudaStream_t s) {
+    static int launch_split(const StageArgs& a, int batch, void* wsp, cudaStream_t s,
+                            const float* htaps = nullptr) {
+        if constexpr (kPT) {
+            if (htaps && pt_fits(a)) {
+                static std::mutex mu;
+                static uint64_t attr_set = 0;
+                static int occ[64] = {0};
+                auto kern = stage_kernel_split_pt<MS, TH, TW, RF_PT, RB, NT, FAST, F, TNRD_PT_MINB, TB>;
+                TB tb;
+                fill_taps(tb, htaps, a.nk);
+                return launch_split_k(kern, CP::smem_bytes(a.tab_stride), a, batch, wsp, s, mu, attr_set,
+                                      occ, tb);
+            }
+        }
         static std::mutex mu;
         static uint64_t attr_set = 0;
         static int occ[64] = {0};
-        const size_t smem = C::smem_bytes(a.tab_stride);
+        auto kern = stage_kernel_split<MS, TH, TW, RF, RB, NT, FAST, F, MINB>;
+        return launch_split_k(kern, C::smem_bytes(a.tab_stride), a, batch, wsp, s, mu, attr_set, occ);
+    }
+
+    template <class K, class... Extra>
+    static int launch_split_k(K kern, size_t smem, const StageArgs& a, int batch, void* wsp,
+                              cudaStream_t s, std::mutex& mu, uint64_t& attr_set, int* occ,
+                              const Extra&... extra) {
         int dev = 0;
         cudaGetDevice(&dev);
-        auto kern = stage_kernel_split<MS, TH, TW, RF, RB, NT, FAST, F, MINB>;
         int rc = prepare(kern, dev, attr_set, mu);
         if (rc) return rc;
         int per_sm = 0, sms = 0;
@@ -720,7 +801,7 @@ struct StageKernel {
         w.part = static_cast<float*>(wsp);
         const long units = (long)w.tiles * b.ngroups;
         const int grid = (int)std::min<long>(units, (long)sms * per_sm);
-        CUDA_TRY(launch_pdl(kern, grid, NT, smem, s, b, w));
+        CUDA_TRY(launch_pdl(kern, grid, NT, smem, s, b, w, extra...));
         const long quads = (long)w.tiles * (TH * TW / 4);
         const int rgrid = (int)std::min<long>((quads + 127) / 128, (long)sms * 16);
         CUDA_TRY(launch_pdl(stage_reduce_kernel<TH, TW>, rgrid, 128, 0, s, b, w));
@@ -768,12 +849,12 @@ static int cc_variant(const StageArgs& a, int batch) {
 }
 
 template <bool FAST, class T>
-static int dispatch_m_t(int m, const StageArgs& a, int batch, cudaStream_t s) {
+static int dispatch_m_t(int m, const StageArgs& a, int batch, cudaStream_t s, const float* htaps = nullptr) {
     switch (m) {
-        case 3: return StageKernel<3, FAST, T>::launch(a, batch, s);
-        case 5: return StageKernel<5, FAST, T>::launch(a, batch, s);
-        case 7: return StageKernel<7, FAST, T>::launch(a, batch, s);
-        case 9: return StageKernel<9, FAST, T>::launch(a, batch, s);
+        case 3: return StageKernel<3, FAST, T>::launch(a, batch, s, htaps);
+        case 5: return StageKernel<5, FAST, T>::launch(a, batch, s, htaps);
+        case 7: return StageKernel<7, FAST, T>::launch(a, batch, s, htaps);
+        case 9: return StageKernel<9, FAST, T>::launch(a, batch, s, htaps);
         default: return fail(TNRD_EUNSUPPORTED, "unsupported filter size %d", m);
     }
 }
@@ -789,12 +870,13 @@ static size_t split_bytes_m_t(int m, const StageArgs& a, int batch) {
 }
 
 template <bool FAST, class T>
-static int dispatch_split_m_t(int m, const StageArgs& a, int batch, void* ws, cudaStream_t s) {
+static int dispatch_split_m_t(int m, const StageArgs& a, int batch, void* ws, cudaStream_t s,
+                              const float* htaps = nullptr) {
     switch (m) {
-        case 3: return StageKernel<3, FAST, T>::launch_split(a, batch, ws, s);
-        case 5: return StageKernel<5, FAST, T>::launch_split(a, batch, ws, s);
-        case 7: return StageKernel<7, FAST, T>::launch_split(a, batch, ws, s);
-        case 9: return StageKernel<9, FAST, T>::launch_split(a, batch, ws, s);
+        case 3: return StageKernel<3, FAST, T>::launch_split(a, batch, ws, s, htaps);
+        case 5: return StageKernel<5, FAST, T>::launch_split(a, batch, ws, s, htaps);
+        case 7: return StageKernel<7, FAST, T>::launch_split(a, batch, ws, s, htaps);
+        case 9: return StageKernel<9, FAST, T>::launch_split(a, batch, ws, s, htaps);
         default: return fail(TNRD_EUNSUPPORTED, "unsupported filter size %d", m);
     }
 }
@@ -825,19 +907,20 @@ template <bool FAST>
 static int dispatch_m(const tnrd_model* md, const StageArgs& a, int batch, cudaStream_t s) {
     const int m = md->m;
     const int v = cc_variant(a, batch);
+    const float* htaps = md->h_taps.data() + (size_t)a.stage * md->nk_pad * md->kp;
     if (v == 0) return dispatch_m_t<FAST, SmallTile>(m, a, batch, s);
-    if (v == 1) return dispatch_m_t<FAST, LargeTile>(m, a, batch, s);
+    if (v == 1) return dispatch_m_t<FAST, LargeTile>(m, a, batch, s, htaps);
     // the split kernel's partials workspace is bounded (it only pays off on
     // small grids anyway)
     if ((v == 2 ? split_bytes_m_t<FAST, SplitTile>(m, a, batch)
                 : split_bytes_m_t<FAST, SmallTile>(m, a, batch)) > kMaxSplitBytes)
-        return dispatch_m_t<FAST, LargeTile>(m, a, batch, s);
+        return dispatch_m_t<FAST, LargeTile>(m, a, batch, s, htaps);
     const size_t bytes = v == 2 ? split_bytes_m_t<FAST, SplitTile>(m, a, batch)
                                 : split_bytes_m_t<FAST, SmallTile>(m, a, batch);
     void* ws = nullptr;
     int rc = split_workspace(md, s, bytes, &ws);
     if (rc) return rc;
-    return v == 2 ? dispatch_split_m_t<FAST, SplitTile>(m, a, batch, ws, s)
+    return v == 2 ? dispatch_split_m_t<FAST, SplitTile>(m, a, batch, ws, s, htaps)
                   : dispatch_split_m_t<FAST, SmallTile>(m, a, batch, ws, s);
 }
 

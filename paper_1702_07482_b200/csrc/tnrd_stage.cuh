@@ -310,77 +310,108 @@ __device__ __forceinline__ void load_taps(const float* tap, float (&k)[C::KK]) {
     }
 }
 
+// forward of one RF x 4 phi block of one filter: z = conv(u, k), phi = rbf(z).
+// K is the filter's taps: a register array (taps staged in shared memory) or
+// a pointer into the kernel's parameter space (TapBlock: warp-uniform, read
+// by the uniform datapath -- LDCU + FFMA with a uniform-register operand --
+// so the taps hold no per-thread registers).
+template <class C, int MS, int RF, bool FAST, int BATCH_ROWS, class K>
+__device__ __forceinline__ void forward_block(const StageArgs& p, const float* sU, float* phif,
+                                              const K& k, uint32_t tb, const float* tabf, int blk) {
+    constexpr int R = C::R;
+    const int by = blk / C::NBX;
+    const int bx = blk - by * C::NBX;
+    const int x0 = bx * 4, y0 = by * RF;
+    float acc[RF][4];
+#pragma unroll
+    for (int r = 0; r < RF; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
+#pragma unroll
+    for (int rr = 0; rr < RF + 2 * R; ++rr) {
+        float v[4 * C::NV];
+        const float* src = sU + (y0 + rr) * C::US + x0;
+#pragma unroll
+        for (int q = 0; q < C::NV; ++q) {
+            const float4 t = lds128(src + 4 * q);
+            v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+        }
+#pragma unroll
+        for (int a = 0; a < MS; ++a) {
+            const int ro = rr - a;
+            if (ro >= 0 && ro < RF) {
+#pragma unroll
+                for (int b = 0; b < MS; ++b) {
+                    // true convolution == correlation with rot180(k)
+                    const float kk = k[(MS - 1 - a) * MS + (MS - 1 - b)];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[ro][c] = fmaf(kk, v[c + b], acc[ro][c]);
+                }
+            }
+        }
+    }
+    float* dst = phif + y0 * C::PW + x0;
+    // BATCH_ROWS = RF: all RF x 4 table lookups before the first phi store
+    // (the lookups are ordered asm loads with a memory clobber, so a
+    // store between rows caps the lookups in flight at one row's four).
+    // Measured on B200: +5% for the tile kernel (C3), -7% for the split
+    // kernel (C2), which therefore stores in smaller row batches.
+    float4 o[RF];
+#pragma unroll
+    for (int r = 0; r < RF; ++r) {
+        if (FAST) {
+            o[r].x = rbf_poly_s(acc[r][0], tb, p);
+            o[r].y = rbf_poly_s(acc[r][1], tb, p);
+            o[r].z = rbf_poly_s(acc[r][2], tb, p);
+            o[r].w = rbf_poly_s(acc[r][3], tb, p);
+        } else {
+            o[r].x = rbf_direct(acc[r][0], tabf, p);
+            o[r].y = rbf_direct(acc[r][1], tabf, p);
+            o[r].z = rbf_direct(acc[r][2], tabf, p);
+            o[r].w = rbf_direct(acc[r][3], tabf, p);
+        }
+        // store rows in batches of BATCH_ROWS (all RF rows: one batch)
+        if ((r + 1) % BATCH_ROWS == 0 || r == RF - 1) {
+#pragma unroll
+            for (int q = r - (r % BATCH_ROWS); q <= r; ++q)
+                *reinterpret_cast<float4*>(dst + q * C::PW) = o[q];
+        }
+    }
+}
+
 // forward: z = conv(u, k) on the phi region, phi = rbf(z); TPF threads per
 // filter, each with the filter's taps in registers
 template <class C, int MS, int RF, int F, bool FAST, int BATCH_ROWS = RF>
 __device__ __forceinline__ void forward_group(const StageArgs& p, const float* sU, float* sPhi,
                                               const float* tapg, const float* tabg, int tid) {
-    constexpr int R = C::R;
     const int fi = tid / C::TPF;
     float k[C::KK];
     load_taps<C>(tapg + fi * C::KP, k);
     const float* tabf = tabg + fi * p.tab_stride;
     const uint32_t tb = rbf_table_base(tabf, p);
     float* phif = sPhi + fi * C::SPHI;
-    for (int blk = tid - fi * C::TPF; blk < C::NBLK; blk += C::TPF) {
-        const int by = blk / C::NBX;
-        const int bx = blk - by * C::NBX;
-        const int x0 = bx * 4, y0 = by * RF;
-        float acc[RF][4];
-#pragma unroll
-        for (int r = 0; r < RF; ++r)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
-#pragma unroll
-        for (int rr = 0; rr < RF + 2 * R; ++rr) {
-            float v[4 * C::NV];
-            const float* src = sU + (y0 + rr) * C::US + x0;
-#pragma unroll
-            for (int q = 0; q < C::NV; ++q) {
-                const float4 t = lds128(src + 4 * q);
-                v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
-            }
-#pragma unroll
-            for (int a = 0; a < MS; ++a) {
-                const int ro = rr - a;
-                if (ro >= 0 && ro < RF) {
-#pragma unroll
-                    for (int b = 0; b < MS; ++b) {
-                        // true convolution == correlation with rot180(k)
-                        const float kk = k[(MS - 1 - a) * MS + (MS - 1 - b)];
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) acc[ro][c] = fmaf(kk, v[c + b], acc[ro][c]);
-                    }
-                }
-            }
-        }
-        float* dst = phif + y0 * C::PW + x0;
-        // BATCH_ROWS = RF: all RF x 4 table lookups before the first phi store
-        // (the lookups are ordered asm loads with a memory clobber, so a
-        // store between rows caps the lookups in flight at one row's four).
-        // Measured on B200: +5% for the tile kernel (C3), -7% for the split
-        // kernel (C2), which therefore stores in smaller row batches.
-        float4 o[RF];
-#pragma unroll
-        for (int r = 0; r < RF; ++r) {
-            if (FAST) {
-                o[r].x = rbf_poly_s(acc[r][0], tb, p);
-                o[r].y = rbf_poly_s(acc[r][1], tb, p);
-                o[r].z = rbf_poly_s(acc[r][2], tb, p);
-                o[r].w = rbf_poly_s(acc[r][3], tb, p);
-            } else {
-                o[r].x = rbf_direct(acc[r][0], tabf, p);
-                o[r].y = rbf_direct(acc[r][1], tabf, p);
-                o[r].z = rbf_direct(acc[r][2], tabf, p);
-                o[r].w = rbf_direct(acc[r][3], tabf, p);
-            }
-            // store rows in batches of BATCH_ROWS (all RF rows: one batch)
-            if ((r + 1) % BATCH_ROWS == 0 || r == RF - 1) {
-#pragma unroll
-                for (int q = r - (r % BATCH_ROWS); q <= r; ++q)
-                    *reinterpret_cast<float4*>(dst + q * C::PW) = o[q];
-            }
-        }
+    for (int blk = tid - fi * C::TPF; blk < C::NBLK; blk += C::TPF)
+        forward_block<C, MS, RF, FAST, BATCH_ROWS>(p, sU, phif, k, tb, tabf, blk);
+}
+
+// forward with the taps in the parameter space: the group's filters one
+// after the other over all NT threads, so the filter (and with it the tap
+// address) is uniform across every warp
+template <class C, int MS, int RF, int F, int NT, bool FAST, int BATCH_ROWS = RF>
+__device__ __forceinline__ void forward_group_pt(const StageArgs& p, const float* sU, float* sPhi,
+                                                 const float* kg, const float* tabg, int tid) {
+#pragma unroll 1
+    for (int fi = 0; fi < F; ++fi) {
+        const float* k = kg + fi * C::KP;
+        const float* tabf = tabg + fi * p.tab_stride;
+        const uint32_t tb = rbf_table_base(tabf, p);
+        float* phif = sPhi + fi * C::SPHI;
+        // warp-uniform control flow (the uniform datapath is only used
+        // outside divergent branches): threads past the last block recompute
+        // it and store the same values
+#pragma unroll 1
+        for (int b0 = 0; b0 < C::NBLK; b0 += NT)
+            forward_block<C, MS, RF, FAST, BATCH_ROWS>(p, sU, phif, k, tb, tabf, min(b0 + tid, C::NBLK - 1));
     }
 }
 
@@ -434,39 +465,57 @@ __device__ __forceinline__ void fix_phi(const StageArgs& p, float* sPhi, int Y0,
     __syncthreads();
 }
 
-// backward: force += corr(phi_i, k_i) for this thread's filters of the group
-template <class C, int MS, int RB, int F>
-__device__ __forceinline__ void backward_group(const float* sPhi, const float* tapg, int split,
-                                               int ox0, int oy0, float (&force)[RB][4]) {
+// backward of one filter: force += corr(phi_i, k_i) over this thread's
+// RB x 4 output block (K: register taps or a parameter-space pointer)
+template <class C, int MS, int RB, class K>
+__device__ __forceinline__ void backward_filter(const float* ph, const K& k, int ox0, int oy0,
+                                                float (&force)[RB][4]) {
     constexpr int R = C::R;
-#pragma unroll 1
-    for (int fi = split; fi < F; fi += C::NSPLIT) {
-        float k[C::KK];
-        load_taps<C>(tapg + fi * C::KP, k);
-        const float* ph = sPhi + fi * C::SPHI;
 #pragma unroll
-        for (int rr = 0; rr < RB + 2 * R; ++rr) {
-            float v[4 * C::NV];
-            const float* src = ph + (oy0 + rr) * C::PW + ox0;
+    for (int rr = 0; rr < RB + 2 * R; ++rr) {
+        float v[4 * C::NV];
+        const float* src = ph + (oy0 + rr) * C::PW + ox0;
 #pragma unroll
-            for (int q = 0; q < C::NV; ++q) {
-                const float4 t = lds128(src + 4 * q);
-                v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
-            }
+        for (int q = 0; q < C::NV; ++q) {
+            const float4 t = lds128(src + 4 * q);
+            v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+        }
 #pragma unroll
-            for (int a = 0; a < MS; ++a) {
-                const int ro = rr - a;
-                if (ro >= 0 && ro < RB) {
+        for (int a = 0; a < MS; ++a) {
+            const int ro = rr - a;
+            if (ro >= 0 && ro < RB) {
 #pragma unroll
-                    for (int b = 0; b < MS; ++b) {
-                        const float kk = k[a * MS + b];
+                for (int b = 0; b < MS; ++b) {
+                    const float kk = k[a * MS + b];
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) force[ro][c] = fmaf(kk, v[c + b], force[ro][c]);
-                    }
+                    for (int c = 0; c < 4; ++c) force[ro][c] = fmaf(kk, v[c + b], force[ro][c]);
                 }
             }
         }
     }
+}
+
+// backward: force += corr(phi_i, k_i) for this thread's filters of the group
+template <class C, int MS, int RB, int F>
+__device__ __forceinline__ void backward_group(const float* sPhi, const float* tapg, int split,
+                                               int ox0, int oy0, float (&force)[RB][4]) {
+#pragma unroll 1
+    for (int fi = split; fi < F; fi += C::NSPLIT) {
+        float k[C::KK];
+        load_taps<C>(tapg + fi * C::KP, k);
+        backward_filter<C, MS, RB>(sPhi + fi * C::SPHI, k, ox0, oy0, force);
+    }
+}
+
+// backward with parameter-space taps (no filter split: every thread walks
+// all of the group's filters, so the tap address is CTA-uniform)
+template <class C, int MS, int RB, int F>
+__device__ __forceinline__ void backward_group_pt(const float* sPhi, const float* kg, int ox0, int oy0,
+                                                  float (&force)[RB][4]) {
+    static_assert(C::NSPLIT == 1, "parameter-space taps need one thread per output block");
+#pragma unroll
+    for (int fi = 0; fi < F; ++fi)
+        backward_filter<C, MS, RB>(sPhi + fi * C::SPHI, kg + fi * C::KP, ox0, oy0, force);
 }
 
 // sum the filter-split partial forces into the split-0 threads (in split
@@ -541,9 +590,52 @@ __device__ __forceinline__ void report(const StageArgs& p, bool bad, uint32_t fb
     if (fbits) atomicAnd(p.status + 1, ~fbits);
 }
 
+
+// ---- RBF tables by bulk copy (TMA engine) ----------------------------------
+// The parameter-space-taps kernels fetch a group's RBF tables with one
+// cp.async.bulk issued by one thread and completed on an mbarrier: no
+// per-thread copy loop in the group loop (which makes ptxas keep the group
+// index, and with it the tap addresses, out of the uniform datapath).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// one thread: dst[0, n) <- src[0, n) (16-byte aligned, n % 4 == 0), completing on bar
+__device__ __forceinline__ void tbar_fetch(float* dst, const float* src, int n, uint64_t* bar) {
+    const uint32_t bytes = 4u * (uint32_t)n;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the generic reads of dst
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+// bounded wait: a lost completion traps instead of hanging the GPU
+__device__ __forceinline__ void tbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_addr(bar);
+    for (uint32_t spin = 0;; ++spin) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n\t}\n"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (spin > (1u << 26)) __trap();
+    }
+}
+
 // ---- tile kernel: one CTA = one output tile, all filter groups -------------
-template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB>
-__global__ void __launch_bounds__(NT, MINB) stage_kernel(const StageArgs p) {
+// PT: taps read from the parameter space (`kp` = this stage's TapBlock)
+// instead of being staged in shared memory and held in registers
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, bool PT>
+__device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float* kp) {
     using C = StageCfg<MS, TH, TW, RF, RB, NT, F>;
     constexpr int R = C::R;
     extern __shared__ __align__(16) float smem[];
@@ -563,12 +655,22 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const StageArgs p) {
     const bool top_halo = p.flags & 0x2u;
     const bool bot_halo = p.flags & 0x4u;
 
-    prefetch_group<C, F, NT>(p, sTap, sTab, 0, 0, tid);
+    __shared__ __align__(8) uint64_t tbar[2];  // PT: RBF table buffers
+    if constexpr (PT) {
+        if (tid == 0) {
+            tbar_init(&tbar[0]);
+            tbar_init(&tbar[1]);
+            tbar_fetch(sTab, p.tab, tabsz, &tbar[0]);
+        }
+        __syncthreads();  // barriers initialised before anyone waits
+    } else {
+        prefetch_group<C, F, NT>(p, sTap, sTab, 0, 0, tid);
+    }
     pdl_wait();     // the previous stage wrote u_in
     pdl_trigger();
     stage_u_tile<C, NT>(p, sU, uin, Y0, X0, top_halo, bot_halo, tid);
 
-    const int split = tid / (C::OBX * C::OBY);            // which filters of a group
+    const int split = PT ? 0 : tid / (C::OBX * C::OBY);  // which filters of a group
     const int obx = tid % C::OBX, oby = (tid / C::OBX) % C::OBY;
     const int ox0 = obx * 4, oy0 = oby * RB;
     float force[RB][4];
@@ -579,15 +681,24 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const StageArgs p) {
 
     for (int g = 0; g < p.ngroups; ++g) {
         const int buf = g & 1;
-        cp_async_wait_all();
+        if constexpr (PT) tbar_wait(&tbar[buf], (g >> 1) & 1);
+        else cp_async_wait_all();
         __syncthreads();  // params of group g landed; previous bwd done with sPhi
-        if (g + 1 < p.ngroups) prefetch_group<C, F, NT>(p, sTap, sTab, g + 1, buf ^ 1, tid);
-        const float* tapg = sTap + buf * F * C::KP;
+        if (g + 1 < p.ngroups) {
+            if constexpr (PT) {
+                if (tid == 0) tbar_fetch(sTab + (buf ^ 1) * tabsz, p.tab + (size_t)(g + 1) * tabsz, tabsz, &tbar[buf ^ 1]);
+            } else {
+                prefetch_group<C, F, NT>(p, sTap, sTab, g + 1, buf ^ 1, tid);
+            }
+        }
+        const float* tapg = PT ? kp + g * F * C::KP : sTap + buf * F * C::KP;
         const float* tabg = sTab + buf * tabsz;
-        forward_group<C, MS, RF, F, FAST>(p, sU, sPhi, tapg, tabg, tid);
+        if constexpr (PT) forward_group_pt<C, MS, RF, F, NT, FAST>(p, sU, sPhi, tapg, tabg, tid);
+        else forward_group<C, MS, RF, F, FAST>(p, sU, sPhi, tapg, tabg, tid);
         __syncthreads();
         fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
-        backward_group<C, MS, RB, F>(sPhi, tapg, split, ox0, oy0, force);
+        if constexpr (PT) backward_group_pt<C, MS, RB, F>(sPhi, tapg, ox0, oy0, force);
+        else backward_group<C, MS, RB, F>(sPhi, tapg, split, ox0, oy0, force);
     }
     if (!reduce_splits<C, RB>(sPhi, split, obx, oby, force)) return;
 
@@ -606,6 +717,26 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel(const StageArgs p) {
         }
     }
     report(p, bad, fbits);
+}
+
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB>
+__global__ void __launch_bounds__(NT, MINB) stage_kernel(const StageArgs p) {
+    stage_tile_body<MS, TH, TW, RF, RB, NT, FAST, F, false>(p, nullptr);
+}
+
+// taps of one stage in the kernel parameter space (<= 32 KB of parameters
+// on sm_100): read with warp-uniform addresses by the uniform datapath, they
+// cost no shared-memory traffic and no per-thread registers
+constexpr int kMaxParamTaps = 7680;
+template <int N>
+struct TapBlock {
+    static_assert(N <= kMaxParamTaps, "kernel parameters are limited to 32 KB");
+    float k[N];
+};
+
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB, class TB>
+__global__ void __launch_bounds__(NT, MINB) stage_kernel_pt(const StageArgs p, const __grid_constant__ TB tk) {
+    stage_tile_body<MS, TH, TW, RF, RB, NT, FAST, F, true>(p, tk.k);
 }
 
 // ---- split kernels: work units = (tile, filter group) ----------------------
@@ -642,8 +773,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
-template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB>
-__global__ void __launch_bounds__(NT, MINB) stage_kernel_split(const StageArgs p, const SplitWs ws) {
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F>
+__device__ __forceinline__ void stage_split_body(const StageArgs& p, const SplitWs& ws) {
 #ifdef TNRD_SPLIT_TRACE
     const unsigned long long tr_t0 = gtimer();
 #endif
@@ -718,6 +849,89 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel_split(const StageArgs p
         g_split_trace[blockIdx.x][3] = (unsigned long long)(uend - ubeg) | ((unsigned long long)(unsigned)ubeg << 32);
     }
 #endif
+}
+
+// split kernel with parameter-space taps: the same units and summation
+// order, walked as tile segments (u staged in the outer loop) so that the
+// inner group loop holds only shared-memory traffic and the partial store:
+// ptxas then keeps the group index -- and the tap addresses -- uniform.
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F>
+__device__ __forceinline__ void stage_split_body_pt(const StageArgs& p, const SplitWs& ws, const float* kp) {
+    using C = StageCfg<MS, TH, TW, RF, RB, NT, F>;
+    constexpr int TPX = TH * TW;
+    extern __shared__ __align__(16) float smem[];
+    float* sU = smem;
+    float* sPhi = sU + C::SU;
+    float* sTab = sPhi + F * C::SPHI + 2 * F * C::KP;
+    const int tabsz = F * p.tab_stride;
+    const int tid = threadIdx.x;
+    const int ng = p.ngroups;
+    const bool top_halo = p.flags & 0x2u;
+    const bool bot_halo = p.flags & 0x4u;
+
+    const int units = ws.tiles * ng;
+    const int nb = units / (int)gridDim.x, extra = units % (int)gridDim.x;
+    const int c = blockIdx.x;
+    const int ubeg = c * nb + min(c, extra);
+    const int nunits = nb + (c < extra ? 1 : 0);
+    const int obx = tid % C::OBX, oby = tid / C::OBX;
+    const int ox0 = obx * 4, oy0 = oby * RB;
+
+    __shared__ __align__(8) uint64_t tbar[2];
+    if (tid == 0) {
+        tbar_init(&tbar[0]);
+        tbar_init(&tbar[1]);
+        if (nunits > 0) tbar_fetch(sTab, p.tab + (size_t)(ubeg % ng) * tabsz, tabsz, &tbar[0]);
+    }
+    __syncthreads();  // barriers initialised before anyone waits
+    pdl_wait();       // the previous stage wrote u_in
+    pdl_trigger();    // the reduction may be scheduled as CTAs retire
+    int k = 0;        // units done (table buffer k & 1, its fill (k >> 1))
+    while (k < nunits) {
+        const int unit = ubeg + k;
+        const int tile = unit / ng, g0 = unit - tile * ng;
+        const int gend = min(ng, g0 + (nunits - k));
+        const int img = tile / (ws.tiles_x * ws.tiles_y);
+        const int trem = tile - img * (ws.tiles_x * ws.tiles_y);
+        const int Y0 = (trem / ws.tiles_x) * TH, X0 = (trem % ws.tiles_x) * TW;
+        __syncthreads();  // the previous unit is done with sU
+        stage_u_tile<C, NT>(p, sU, p.u_in + (int64_t)img * p.img_stride, Y0, X0, top_halo, bot_halo, tid);
+        float* dst = ws.part + (size_t)tile * ng * TPX + oy0 * TW + ox0;
+        for (int g = g0; g < gend; ++g, ++k) {
+            const int buf = k & 1;
+            tbar_wait(&tbar[buf], (k >> 1) & 1);
+            __syncthreads();  // table + u tile in smem; previous unit done with sPhi
+            if (tid == 0 && k + 1 < nunits)
+                tbar_fetch(sTab + (buf ^ 1) * tabsz, p.tab + (size_t)(g + 1 < ng ? g + 1 : 0) * tabsz, tabsz,
+                           &tbar[buf ^ 1]);
+            const float* tapg = kp + g * F * C::KP;
+            const float* tabg = sTab + buf * tabsz;
+            forward_group_pt<C, MS, RF, F, NT, FAST, TNRD_SPLIT_RBF_ROWS>(p, sU, sPhi, tapg, tabg, tid);
+            __syncthreads();
+            fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
+            float force[RB][4];
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) force[r][cc] = 0.0f;
+            backward_group_pt<C, MS, RB, F>(sPhi, tapg, ox0, oy0, force);
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+                __stcg(reinterpret_cast<float4*>(dst + (size_t)g * TPX + r * TW),
+                       make_float4(force[r][0], force[r][1], force[r][2], force[r][3]));
+        }
+    }
+}
+
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB>
+__global__ void __launch_bounds__(NT, MINB) stage_kernel_split(const StageArgs p, const SplitWs ws) {
+    stage_split_body<MS, TH, TW, RF, RB, NT, FAST, F>(p, ws);
+}
+
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB, class TB>
+__global__ void __launch_bounds__(NT, MINB) stage_kernel_split_pt(const StageArgs p, const SplitWs ws,
+                                                                 const __grid_constant__ TB tk) {
+    stage_split_body_pt<MS, TH, TW, RF, RB, NT, FAST, F>(p, ws, tk.k);
 }
 
 // sum of a pixel quad's partials in group order, then the epilogue (u from
