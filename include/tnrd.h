@@ -119,6 +119,12 @@ int tnrd_model_rbf_fit(const tnrd_model* model, double* max_abs_err,
  * 3 waves of large tiles; it keeps a partial-force workspace per stream
  * inside the model (allocated on first use, outside stream capture). */
 int tnrd_set_stage_kernel(int mode);
+/* Where the CUDA-core large-tile stage kernels read the filter taps
+ * (process-wide): 1 (default) = the kernel parameter space, read by the
+ * uniform datapath (m <= 7, nk <= 48 with m = 7); 0 = staged in shared memory
+ * and held in registers.  Both give bit-identical results; the initial value
+ * can be set with TNRD_PARAM_TAPS=0|1 in the environment. */
+int tnrd_set_param_taps(int on);
 /* z-field stage precision (process-wide): number of tf32 cross products of
  * the 3-piece splits of u and k -- 6 (default: below fp32 rounding), 4 or 3
  * (experiments). */

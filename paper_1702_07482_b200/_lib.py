@@ -53,6 +53,7 @@ SIGNATURES = {
                                     ctypes.POINTER(_c_dbl),
                                     ctypes.POINTER(_c_int)]),
     "tnrd_set_stage_kernel": (_c_int, [_c_int]),
+    "tnrd_set_param_taps": (_c_int, [_c_int]),
     "tnrd_set_zfield_passes": (_c_int, [_c_int]),
     "tnrd_status_reset": (_c_int, [_vp, _vp]),
     "tnrd_status_decode": (_c_int, [ctypes.POINTER(_c_u32),
@@ -154,6 +155,12 @@ def set_stage_kernel(mode: int) -> None:
     """0 auto, 1 CUDA-core, 2 tcgen05 forward GEMM, 3/4 CUDA-core with
     small/large tiles forced."""
     check(load().tnrd_set_stage_kernel(int(mode)))
+
+
+def set_param_taps(on: bool) -> None:
+    """Large-tile CUDA-core kernels: taps from the kernel parameter space
+    (True, default) or staged in shared memory (False); same bits."""
+    check(load().tnrd_set_param_taps(int(bool(on))))
 
 
 def launch_count() -> int:

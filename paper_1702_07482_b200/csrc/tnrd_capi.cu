@@ -122,6 +122,13 @@ struct tnrd_model {
 // plans: all stages in one launch; opt-in), 8 = z-field stage
 // (tnrd_stage_zf.cuh: tcgen05 forward over the image + TMA-fed RBF/adjoint)
 static std::atomic<int> g_kernel_mode{0};
+// tnrd_set_param_taps; -1 = not set (TNRD_PARAM_TAPS=0|1 gives the initial value)
+static std::atomic<int> g_param_taps{-1};
+
+extern "C" int tnrd_set_param_taps(int on) {
+    g_param_taps.store(on ? 1 : 0);
+    return TNRD_OK;
+}
 
 extern "C" int tnrd_set_stage_kernel(int mode) {
     if (mode < 0 || mode > 9) return fail(TNRD_EINVAL, "stage kernel mode must be in 0..9");
@@ -455,6 +462,9 @@ extern "C" int tnrd_status_decode(const uint32_t* h, int* bad_stage) {
 #ifndef TNRD_PT_RF
 #define TNRD_PT_RF 5
 #endif
+#ifndef TNRD_PT_M9_RF
+#define TNRD_PT_M9_RF 2
+#endif
 #ifndef TNRD_PT_MINB
 #define TNRD_PT_MINB 2
 #endif
@@ -463,17 +473,22 @@ extern "C" int tnrd_status_decode(const uint32_t* h, int* bad_stage) {
 #ifndef TNRD_PT_TILE_F
 #define TNRD_PT_TILE_F 2
 #endif
+#ifndef TNRD_PT_SPLIT_F
+#define TNRD_PT_SPLIT_F 2
+#endif
 #ifndef TNRD_PT_TILE_MINB
 #define TNRD_PT_TILE_MINB 2
 #endif
-// TNRD_PARAM_TAPS=0 in the environment selects the shared-memory-taps
-// kernels (A/B measurements)
 static bool param_taps_enabled() {
-    static const bool on = [] {
+    int v = g_param_taps.load();
+    if (v < 0) {
         const char* e = std::getenv("TNRD_PARAM_TAPS");
-        return !(e && e[0] == '0');
-    }();
-    return on;
+        v = (e && e[0] == '0') ? 0 : 1;
+        int expect = -1;
+        g_param_taps.compare_exchange_strong(expect, v);
+        v = g_param_taps.load();
+    }
+    return v != 0;
 }
 
 struct SmallTile { static constexpr int TH = 32, TW = 32, RF = 2, RB = 2, NT = 256, F = 4; };
@@ -635,14 +650,18 @@ struct StageKernel {
 
     // parameter-space taps (TapBlock, tnrd_stage.cuh): large tiles only (one
     // thread per output block, so the tap address is warp-uniform)
-    // (m <= 7: 81 taps of m = 9 exceed the 63 uniform registers per warp --
-    // measured 19% slower on C5)
-    static constexpr bool kPT = T::TH == 64 && FAST && MS <= 7;
-    using TB = TapBlock<2560>;
-    static constexpr int RF_PT = TNRD_PT_RF;
+    static constexpr bool kPT = T::TH == 64 && FAST;
+    using TB = TapBlock<MS <= 7 ? 2560 : kMaxParamTaps>;
+    // forward blocking (measured on B200): m = 7 RF = 5 (252 blocks per
+    // filter for 256 threads); m = 9 RF = 2 (C5 172.5 MPix/s; RF = 3 167.4,
+    // RF = 6 144.4, RF = 4 138)
+    static constexpr int RF_PT = MS >= 9 ? TNRD_PT_M9_RF : TNRD_PT_RF;
     static constexpr int F_TILE_PT = TNRD_PT_TILE_F;
-    using CP = StageCfg<MS, TH, TW, RF_PT, RB, NT, F>;
     using CPT = StageCfg<MS, TH, TW, RF_PT, RB, NT, F_TILE_PT>;
+    static constexpr int F_SPLIT_PT = TNRD_PT_SPLIT_F;
+    using CPS = StageCfg<MS, TH, TW, RF_PT, RB, NT, F_SPLIT_PT>;
+    // filters per split unit (the parameter-space kernel has its own)
+    static int split_f(const StageArgs& a) { return pt_fits(a) ? F_SPLIT_PT : F; }
     // htaps: this stage's taps on the host, [nk_pad][kp]
     static bool pt_fits(const StageArgs& a) {
         return kPT && param_taps_enabled() &&
@@ -749,7 +768,8 @@ struct StageKernel {
     }
     static size_t ws_bytes(const StageArgs& a, int batch) {
         const long nt = tiles(a, batch);
-        return (size_t)nt * ((a.nk + F - 1) / F) * TH * TW * sizeof(float);
+        const int fs = split_f(a);
+        return (size_t)nt * ((a.nk + fs - 1) / fs) * TH * TW * sizeof(float);
     }
 
     // persistent grid of (SMs x resident CTAs) over (tile, group) units
@@ -760,22 +780,22 @@ struct StageKernel {
                 static std::mutex mu;
                 static uint64_t attr_set = 0;
                 static int occ[64] = {0};
-                auto kern = stage_kernel_split_pt<MS, TH, TW, RF_PT, RB, NT, FAST, F, TNRD_PT_MINB, TB>;
+                auto kern = stage_kernel_split_pt<MS, TH, TW, RF_PT, RB, NT, FAST, F_SPLIT_PT, TNRD_PT_MINB, TB>;
                 TB tb;
                 fill_taps(tb, htaps, a.nk);
-                return launch_split_k(kern, CP::smem_bytes(a.tab_stride), a, batch, wsp, s, mu, attr_set,
-                                      occ, tb);
+                return launch_split_k(kern, CPS::smem_bytes(a.tab_stride), F_SPLIT_PT, a, batch, wsp, s, mu,
+                                      attr_set, occ, tb);
             }
         }
         static std::mutex mu;
         static uint64_t attr_set = 0;
         static int occ[64] = {0};
         auto kern = stage_kernel_split<MS, TH, TW, RF, RB, NT, FAST, F, MINB>;
-        return launch_split_k(kern, C::smem_bytes(a.tab_stride), a, batch, wsp, s, mu, attr_set, occ);
+        return launch_split_k(kern, C::smem_bytes(a.tab_stride), F, a, batch, wsp, s, mu, attr_set, occ);
     }
 
     template <class K, class... Extra>
-    static int launch_split_k(K kern, size_t smem, const StageArgs& a, int batch, void* wsp,
+    static int launch_split_k(K kern, size_t smem, int fgroup, const StageArgs& a, int batch, void* wsp,
                               cudaStream_t s, std::mutex& mu, uint64_t& attr_set, int* occ,
                               const Extra&... extra) {
         int dev = 0;
@@ -793,7 +813,7 @@ struct StageKernel {
         }
         CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         StageArgs b = a;
-        b.ngroups = (a.nk + F - 1) / F;
+        b.ngroups = (a.nk + fgroup - 1) / fgroup;
         SplitWs w;
         w.tiles_x = (a.W + TW - 1) / TW;
         w.tiles_y = (a.H + TH - 1) / TH;
