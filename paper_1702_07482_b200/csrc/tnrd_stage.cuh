@@ -513,9 +513,17 @@ template <class C, int MS, int RB, int F>
 __device__ __forceinline__ void backward_group_pt(const float* sPhi, const float* kg, int ox0, int oy0,
                                                   float (&force)[RB][4]) {
     static_assert(C::NSPLIT == 1, "parameter-space taps need one thread per output block");
-#pragma unroll
-    for (int fi = 0; fi < F; ++fi)
-        backward_filter<C, MS, RB>(sPhi + fi * C::SPHI, kg + fi * C::KP, ox0, oy0, force);
+    // not unrolled (the kernel's hot loop stays within the instruction
+    // cache); written with pointer increments and a __syncwarp, the form in
+    // which ptxas keeps the taps in uniform registers (a plain indexed
+    // unroll-1 loop loads them into per-thread registers with LDC)
+    const float* k = kg;
+    const float* ph = sPhi;
+#pragma unroll 1
+    for (int fi = 0; fi < F; ++fi, k += C::KP, ph += C::SPHI) {
+        backward_filter<C, MS, RB>(ph, k, ox0, oy0, force);
+        __syncwarp();
+    }
 }
 
 // sum the filter-split partial forces into the split-0 threads (in split
