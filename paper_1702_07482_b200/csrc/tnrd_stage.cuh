@@ -914,7 +914,9 @@ __device__ __forceinline__ void stage_split_body_pt(const StageArgs& p, const Sp
                            &tbar[buf ^ 1]);
             const float* tapg = kp + g * F * C::KP;
             const float* tabg = sTab + buf * tabsz;
-            forward_group_pt<C, MS, RF, F, NT, FAST, TNRD_SPLIT_RBF_ROWS>(p, sU, sPhi, tapg, tabg, tid);
+            // all RF rows' table lookups before the phi stores (with the taps
+            // out of the registers this pays here too: +1% C2 on B200)
+            forward_group_pt<C, MS, RF, F, NT, FAST>(p, sU, sPhi, tapg, tabg, tid);
             __syncthreads();
             fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
             float force[RB][4];
