@@ -102,6 +102,13 @@ int tnrd_model_info(const tnrd_model* model, int* m, int* nk, int* T, int* M,
 int tnrd_model_rbf_fit(const tnrd_model* model, double* max_abs_err,
                        double* max_abs_err_fp32, double* max_sum_abs_w,
                        int* intervals);
+/* Same for the cubic table the parameter-space-taps kernels evaluate
+ * (intervals of width min(delta, gamma) / 10, one float4 of monomial
+ * coefficients each): max |p - phi| with float64 and with the fp32
+ * coefficients, and the number of intervals (0 = no cubic table: those
+ * kernels are not used for this model). */
+int tnrd_model_rbf_fit_cubic(const tnrd_model* model, double* max_abs_err,
+                             double* max_abs_err_fp32, int* intervals);
 
 /* Stage kernel selection (process-wide): 0 = auto (the kernel measured
  * fastest on B200 for the grid size), 1 = CUDA-core kernels

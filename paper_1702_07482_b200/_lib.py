@@ -48,6 +48,8 @@ SIGNATURES = {
     "tnrd_model_destroy": (_c_int, [_vp]),
     "tnrd_model_set_variant": (_c_int, [_vp, _c_int, _c_dbl]),
     "tnrd_model_info": (_c_int, [_vp] + [ctypes.POINTER(_c_int)] * 5),
+    "tnrd_model_rbf_fit_cubic": (_c_int, [_vp, ctypes.POINTER(_c_dbl), ctypes.POINTER(_c_dbl),
+                                         ctypes.POINTER(_c_int)]),
     "tnrd_model_rbf_fit": (_c_int, [_vp, ctypes.POINTER(_c_dbl),
                                     ctypes.POINTER(_c_dbl),
                                     ctypes.POINTER(_c_dbl),

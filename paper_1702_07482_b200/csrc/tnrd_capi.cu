@@ -18,6 +18,7 @@
 #include <mutex>
 #include <type_traits>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/tnrd.h"
@@ -86,6 +87,13 @@ struct tnrd_model {
     double fit_err = 0;     // max |p(z) - phi(z)| over all filters/stages
     double fit_err32 = 0;   // same with the fp32 coefficients
     double fit_scale = 0;   // max sum_j |w_ij|
+    // cubic RBF table of the parameter-space-taps kernels (tnrd_stage.cuh
+    // rbf_cubic_s): intervals of width h3 = min(delta, gamma) / kCubicSub,
+    // one float4 (c0..c3) each
+    double h3 = 0;
+    int ni3 = 0, tab3_stride = 0;
+    double fit_err3 = 0, fit_err3_32 = 0;
+    float* d_tab3 = nullptr;  // T * nk_pad * tab3_stride
     std::vector<double> lam;
     int variant = 0;          // 0 prox, 1 projected (tnrd_model_set_variant)
     double floor = 1.0;       // projection floor
@@ -167,9 +175,9 @@ static double phi_exact(const double* w, int M, double mu0, double delta, double
 // Returns the max abs interpolation error (float64 coefficients) over 41
 // check points and, in *err32, the same with the fp32-rounded coefficients
 // the kernel uses.
+template <int N = kPolyN, int NCHECK = 41>
 static double fit_interval(const double* w, int M, double mu0, double delta, double gamma,
                            double zc, double h, float* out, double* err32) {
-    constexpr int N = kPolyDeg + 1;
     long double A[N][N + 1];
     for (int k = 0; k < N; ++k) {
         const long double x = 0.5L * std::cos(M_PI * (2 * k + 1) / (2.0 * N));
@@ -194,11 +202,12 @@ static double fit_interval(const double* w, int M, double mu0, double delta, dou
     for (int d = 0; d < N; ++d) {
         c[d] = (double)(A[d][N] / A[d][d]);
         c32[d] = (float)c[d];
-        out[(d >> 2) * 32 + (d & 3)] = c32[d];   // c0..c3 | c4..c7 at +32 floats (rbf_lo_offset)
+        // degree 7: c0..c3 | c4..c7 at +32 floats (rbf_lo_offset); cubic: c0..c3
+        out[N == 8 ? (d >> 2) * 32 + (d & 3) : d] = c32[d];
     }
     double err = 0.0, e32 = 0.0;
-    for (int k = 0; k <= 40; ++k) {
-        const double x = -0.5 + k / 40.0;
+    for (int k = 0; k < NCHECK; ++k) {
+        const double x = -0.5 + k / (double)(NCHECK - 1);
         double acc = 0.0, acc32 = 0.0;
         for (int d = N - 1; d >= 0; --d) {
             acc = acc * x + c[d];
@@ -256,9 +265,16 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
     md->fast = (size_t)md->nip * kPolyN * kF <= 16384;  // <= 64 KB per group buffer
     md->tab_stride = md->fast ? md->nip * kPolyN : round_up(M, 4);
 
+    // cubic table (parameter-space-taps kernels): same range, h / 5
+    md->h3 = std::min(delta, gamma) / kCubicSub;
+    md->ni3 = (int)std::ceil((zhi - md->zlo) / md->h3) + 1;
+    md->tab3_stride = md->fast ? round_up(md->ni3, 8) * 4 : 0;
+    if (md->tab3_stride > kMaxCubicStride) md->tab3_stride = 0;   // PT kernels off
+
     const size_t ntap = (size_t)T * md->nk_pad * md->kp;
     const size_t ntab = (size_t)T * md->nk_pad * md->tab_stride;
-    std::vector<float> taps(ntap, 0.0f), tab(ntab, 0.0f);
+    const size_t ntab3 = (size_t)T * md->nk_pad * md->tab3_stride;
+    std::vector<float> taps(ntap, 0.0f), tab(ntab, 0.0f), tab3(ntab3, 0.0f);
     for (int t = 0; t < T; ++t) {
         for (int i = 0; i < nk; ++i) {
             const double* k = kernels + ((size_t)t * nk + i) * m * m;
@@ -281,6 +297,33 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
             } else {
                 for (int j = 0; j < M; ++j) tb[j] = (float)w[j];
             }
+        }
+    }
+    if (md->tab3_stride) {
+        // (stage, filter) fits on all host threads
+        const int jobs = T * nk;
+        const int nth = std::max(1, std::min<int>(jobs, (int)std::thread::hardware_concurrency()));
+        std::vector<double> e3(nth, 0.0), e3_32(nth, 0.0);
+        std::vector<std::thread> th;
+        for (int id = 0; id < nth; ++id)
+            th.emplace_back([&, id] {
+                for (int job = id; job < jobs; job += nth) {
+                    const int t = job / nk, i = job % nk;
+                    const double* w = weights + ((size_t)t * nk + i) * M;
+                    float* tb = tab3.data() + ((size_t)t * md->nk_pad + i) * md->tab3_stride;
+                    for (int q = 0; q < md->ni3; ++q) {
+                        double e32 = 0.0;
+                        e3[id] = std::max(e3[id], fit_interval<4, 9>(w, M, mu0, delta, gamma,
+                                                                    md->zlo + q * md->h3, md->h3,
+                                                                    tb + 4 * q, &e32));
+                        e3_32[id] = std::max(e3_32[id], e32);
+                    }
+                }
+            });
+        for (auto& x : th) x.join();
+        for (int id = 0; id < nth; ++id) {
+            md->fit_err3 = std::max(md->fit_err3, e3[id]);
+            md->fit_err3_32 = std::max(md->fit_err3_32, e3_32[id]);
         }
     }
     // forward GEMM operand for the tensor-core kernel (kf = rot180(k), split
@@ -362,16 +405,27 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
         cudaError_t e1 = cudaMalloc(&md->d_taps, ntap * sizeof(float));
         cudaError_t e2 = cudaMalloc(&md->d_tab, ntab * sizeof(float));
         if (e1 != cudaSuccess || e2 != cudaSuccess) {
-            cudaFree(md->d_taps); cudaFree(md->d_tab); cudaFree(md->d_bop); cudaFree(md->d_zop);
+            cudaFree(md->d_taps); cudaFree(md->d_tab); cudaFree(md->d_tab3); cudaFree(md->d_bop); cudaFree(md->d_zop);
             delete md;
             return fail(TNRD_ECUDA, "cudaMalloc of model parameters failed: %s",
                         cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
         }
         md->h_taps.assign(taps.begin(), taps.begin() + ntap);
+        if (ntab3) {
+            cudaError_t e5 = cudaMalloc(&md->d_tab3, ntab3 * sizeof(float));
+            if (e5 == cudaSuccess)
+                e5 = cudaMemcpy(md->d_tab3, tab3.data(), ntab3 * sizeof(float), cudaMemcpyHostToDevice);
+            if (e5 != cudaSuccess) {
+                cudaFree(md->d_taps); cudaFree(md->d_tab); cudaFree(md->d_tab3); cudaFree(md->d_bop);
+                cudaFree(md->d_zop);
+                delete md;
+                return fail(TNRD_ECUDA, "cubic RBF table upload failed: %s", cudaGetErrorString(e5));
+            }
+        }
         cudaError_t e3 = cudaMemcpy(md->d_taps, taps.data(), ntap * sizeof(float), cudaMemcpyHostToDevice);
         cudaError_t e4 = cudaMemcpy(md->d_tab, tab.data(), ntab * sizeof(float), cudaMemcpyHostToDevice);
         if (e3 != cudaSuccess || e4 != cudaSuccess) {
-            cudaFree(md->d_taps); cudaFree(md->d_tab); cudaFree(md->d_bop); cudaFree(md->d_zop);
+            cudaFree(md->d_taps); cudaFree(md->d_tab); cudaFree(md->d_tab3); cudaFree(md->d_bop); cudaFree(md->d_zop);
             delete md;
             return fail(TNRD_ECUDA, "parameter upload failed: %s",
                         cudaGetErrorString(e3 != cudaSuccess ? e3 : e4));
@@ -387,6 +441,7 @@ extern "C" int tnrd_model_destroy(tnrd_model* md) {
         DeviceGuard dg(md->device);
         cudaFree(md->d_taps);
         cudaFree(md->d_tab);
+        cudaFree(md->d_tab3);
         cudaFree(md->d_bop);
         cudaFree(md->d_zop);
         for (auto& kv : md->ws) cudaFree(kv.second.ptr);
@@ -405,6 +460,15 @@ extern "C" int tnrd_model_rbf_fit(const tnrd_model* md, double* max_abs_err,
     if (max_abs_err_fp32) *max_abs_err_fp32 = md->fit_err32;
     if (max_sum_abs_w) *max_sum_abs_w = md->fit_scale;
     if (intervals) *intervals = md->fast ? md->ni : 0;
+    return TNRD_OK;
+}
+
+extern "C" int tnrd_model_rbf_fit_cubic(const tnrd_model* md, double* max_abs_err,
+                                        double* max_abs_err_fp32, int* intervals) {
+    if (!md) return fail(TNRD_EINVAL, "model is NULL");
+    if (max_abs_err) *max_abs_err = md->fit_err3;
+    if (max_abs_err_fp32) *max_abs_err_fp32 = md->fit_err3_32;
+    if (intervals) *intervals = md->tab3_stride ? md->ni3 : 0;
     return TNRD_OK;
 }
 
@@ -664,8 +728,13 @@ struct StageKernel {
     static int split_f(const StageArgs& a) { return pt_fits(a) ? F_SPLIT_PT : F; }
     // htaps: this stage's taps on the host, [nk_pad][kp]
     static bool pt_fits(const StageArgs& a) {
-        return kPT && param_taps_enabled() &&
+        return kPT && param_taps_enabled() && a.tab3 != nullptr &&
                (size_t)round_up(a.nk, 4) * C::KP <= sizeof(TB) / sizeof(float);
+    }
+    // shared memory of the PT kernels: u | phi[f] | one cubic table for f filters
+    template <class CC, int FF>
+    static size_t pt_smem(const StageArgs& a) {
+        return sizeof(float) * ((size_t)CC::SU + (size_t)FF * CC::SPHI + (size_t)FF * a.tab3_stride);
     }
     static void fill_taps(TB& tb, const float* htaps, int nk) {
         std::memcpy(tb.k, htaps, sizeof(float) * (size_t)round_up(nk, 4) * C::KP);
@@ -689,7 +758,7 @@ struct StageKernel {
                 TB tb;
                 fill_taps(tb, htaps, a.nk);
                 b.ngroups = (a.nk + F_TILE_PT - 1) / F_TILE_PT;
-                CUDA_TRY(launch_pdl(kern, grid, NT, CPT::smem_bytes(a.tab_stride), s, b, tb));
+                CUDA_TRY(launch_pdl(kern, grid, NT, pt_smem<CPT, F_TILE_PT>(a), s, b, tb));
                 g_launches.fetch_add(1);
                 return TNRD_OK;
             }
@@ -783,7 +852,7 @@ struct StageKernel {
                 auto kern = stage_kernel_split_pt<MS, TH, TW, RF_PT, RB, NT, FAST, F_SPLIT_PT, TNRD_PT_MINB, TB>;
                 TB tb;
                 fill_taps(tb, htaps, a.nk);
-                return launch_split_k(kern, CPS::smem_bytes(a.tab_stride), F_SPLIT_PT, a, batch, wsp, s, mu,
+                return launch_split_k(kern, pt_smem<CPS, F_SPLIT_PT>(a), F_SPLIT_PT, a, batch, wsp, s, mu,
                                       attr_set, occ, tb);
             }
         }
@@ -1280,6 +1349,12 @@ static StageArgs stage_args(const tnrd_model* md, int t, uint32_t flags) {
     a.tab_ni = md->nip;
     a.t_off = (float)(-md->zlo / md->h);
     a.tmax = (float)(md->ni - 1);
+    a.tab3 = md->tab3_stride ? md->d_tab3 + (size_t)t * md->nk_pad * md->tab3_stride : nullptr;
+    a.tab3_stride = md->tab3_stride;
+    a.tab3_bias = 0u - (0x4B400000u << 4);
+    a.inv_h3 = md->tab3_stride ? (float)(1.0 / md->h3) : 0.0f;
+    a.t_off3 = md->tab3_stride ? (float)(-md->zlo / md->h3) : 0.0f;
+    a.tmax3 = (float)(md->ni3 - 1);
     a.delta = (float)md->delta;
     a.cE = (float)(-L2E / (2.0 * md->gamma * md->gamma));
     a.mu0 = (float)md->mu0;

@@ -40,6 +40,12 @@ constexpr int kF = 4;          // filters per group
 constexpr int kPolyDeg = 7;    // RBF interpolant degree per interval
 constexpr int kPolyN = kPolyDeg + 1;  // coefficients per interval
 constexpr int kPolySub = 2;    // intervals per min(delta, gamma)
+// cubic table (parameter-space-taps kernels, rbf_cubic_s): 10 intervals per
+// min(delta, gamma): interpolation error ~1e-7 of sum|w| (fp32 resolution
+// of phi); at most kMaxCubicStride floats per filter (a single-buffered
+// 2-filter group table then fits beside 2 CTAs per SM)
+constexpr double kCubicSub = 10.0;
+constexpr int kMaxCubicStride = 4096;
 constexpr float kFFloor = 1e-6f;  // speckle.py:21
 
 __host__ __device__ constexpr int round_up(int x, int a) { return (x + a - 1) / a * a; }
@@ -78,6 +84,13 @@ struct StageArgs {
     int tab_ni;
     float t_off;
     float tmax;
+    // RBF: cubic table (parameter-space-taps kernels): interval j at tab3[4 j]
+    const float* tab3;   // [nk_pad][tab3_stride]
+    int tab3_stride;     // floats per filter (0: no cubic table)
+    uint32_t tab3_bias;  // -(0x4B400000 << 4) mod 2^32
+    float inv_h3;
+    float t_off3;
+    float tmax3;
     // RBF: direct all-centre sum (fallback for very large tables)
     float delta;
     float cE;            // -log2(e) / (2 gamma^2)
@@ -208,6 +221,26 @@ __device__ __forceinline__ float rbf_poly_s(float z, uint32_t tb, const StageArg
     return rbf_horner(x, lo, hi);
 }
 
+// cubic table (parameter-space-taps kernels): interval j = one float4
+// c0..c3 at tb3 + 16 j bytes (`tb3` = the table's shared address +
+// p.tab3_bias); 8 lanes with consecutive intervals hit 8 distinct bank
+// quads.  One 128-bit load + 3 FFMA per response (the degree-7 table needs
+// two loads + 7 FFMA; measured on B200 the second load's latency, not the
+// FFMAs, is what the forward waits on).
+__device__ __forceinline__ float rbf_cubic_s(float z, uint32_t tb3, const StageArgs& p) {
+    float t = fmaf(z, p.inv_h3, p.t_off3);
+    t = fminf(fmaxf(t, 0.0f), p.tmax3);
+    const float r = t + 12582912.0f;
+    const float x = t - (r - 12582912.0f);
+    const uint32_t a = (static_cast<uint32_t>(__float_as_int(r)) << 4) + tb3;
+    float4 c;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(c.x), "=f"(c.y), "=f"(c.z), "=f"(c.w)
+                 : "r"(a)
+                 : "memory");
+    return fmaf(fmaf(fmaf(c.w, x, c.z), x, c.y), x, c.x);
+}
+
 // phi(z) as the reference writes it: all M centres (generic bandwidths).
 __device__ __forceinline__ float rbf_direct(float z, const float* __restrict__ w,
                                             const StageArgs& p) {
@@ -315,7 +348,7 @@ __device__ __forceinline__ void load_taps(const float* tap, float (&k)[C::KK]) {
 // a pointer into the kernel's parameter space (TapBlock: warp-uniform, read
 // by the uniform datapath -- LDCU + FFMA with a uniform-register operand --
 // so the taps hold no per-thread registers).
-template <class C, int MS, int RF, bool FAST, int BATCH_ROWS, class K>
+template <class C, int MS, int RF, bool FAST, int BATCH_ROWS, bool CUBIC = false, class K>
 __device__ __forceinline__ void forward_block(const StageArgs& p, const float* sU, float* phif,
                                               const K& k, uint32_t tb, const float* tabf, int blk) {
     constexpr int R = C::R;
@@ -359,7 +392,12 @@ __device__ __forceinline__ void forward_block(const StageArgs& p, const float* s
     float4 o[RF];
 #pragma unroll
     for (int r = 0; r < RF; ++r) {
-        if (FAST) {
+        if (CUBIC) {
+            o[r].x = rbf_cubic_s(acc[r][0], tb, p);
+            o[r].y = rbf_cubic_s(acc[r][1], tb, p);
+            o[r].z = rbf_cubic_s(acc[r][2], tb, p);
+            o[r].w = rbf_cubic_s(acc[r][3], tb, p);
+        } else if (FAST) {
             o[r].x = rbf_poly_s(acc[r][0], tb, p);
             o[r].y = rbf_poly_s(acc[r][1], tb, p);
             o[r].z = rbf_poly_s(acc[r][2], tb, p);
@@ -403,15 +441,15 @@ __device__ __forceinline__ void forward_group_pt(const StageArgs& p, const float
 #pragma unroll 1
     for (int fi = 0; fi < F; ++fi) {
         const float* k = kg + fi * C::KP;
-        const float* tabf = tabg + fi * p.tab_stride;
-        const uint32_t tb = rbf_table_base(tabf, p);
+        const float* tabf = tabg + fi * p.tab3_stride;
+        const uint32_t tb = static_cast<uint32_t>(__cvta_generic_to_shared(tabf)) + p.tab3_bias;
         float* phif = sPhi + fi * C::SPHI;
         // warp-uniform control flow (the uniform datapath is only used
         // outside divergent branches): threads past the last block recompute
         // it and store the same values
 #pragma unroll 1
         for (int b0 = 0; b0 < C::NBLK; b0 += NT)
-            forward_block<C, MS, RF, FAST, BATCH_ROWS>(p, sU, phif, k, tb, tabf, min(b0 + tid, C::NBLK - 1));
+            forward_block<C, MS, RF, FAST, BATCH_ROWS, true>(p, sU, phif, k, tb, tabf, min(b0 + tid, C::NBLK - 1));
     }
 }
 
@@ -649,9 +687,10 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
     extern __shared__ __align__(16) float smem[];
     float* sU = smem;
     float* sPhi = sU + C::SU;
+    // PT: no tap buffer, one (cubic) table buffer: u | phi[F] | tab3[F]
     float* sTap = sPhi + F * C::SPHI;
-    float* sTab = sTap + 2 * F * C::KP;
-    const int tabsz = F * p.tab_stride;
+    float* sTab = PT ? sTap : sTap + 2 * F * C::KP;
+    const int tabsz = F * (PT ? p.tab3_stride : p.tab_stride);
 
     const int tid = threadIdx.x;
     const int img = blockIdx.z;
@@ -663,14 +702,13 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
     const bool top_halo = p.flags & 0x2u;
     const bool bot_halo = p.flags & 0x4u;
 
-    __shared__ __align__(8) uint64_t tbar[2];  // PT: RBF table buffers
+    __shared__ __align__(8) uint64_t tbar;  // PT: the table buffer's fills
     if constexpr (PT) {
         if (tid == 0) {
-            tbar_init(&tbar[0]);
-            tbar_init(&tbar[1]);
-            tbar_fetch(sTab, p.tab, tabsz, &tbar[0]);
+            tbar_init(&tbar);
+            tbar_fetch(sTab, p.tab3, tabsz, &tbar);
         }
-        __syncthreads();  // barriers initialised before anyone waits
+        __syncthreads();  // barrier initialised before anyone waits
     } else {
         prefetch_group<C, F, NT>(p, sTap, sTab, 0, 0, tid);
     }
@@ -688,22 +726,20 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
         for (int c = 0; c < 4; ++c) force[r][c] = 0.0f;
 
     for (int g = 0; g < p.ngroups; ++g) {
-        const int buf = g & 1;
-        if constexpr (PT) tbar_wait(&tbar[buf], (g >> 1) & 1);
+        const int buf = PT ? 0 : g & 1;
+        if constexpr (PT) tbar_wait(&tbar, g & 1);  // fill g of the one buffer
         else cp_async_wait_all();
         __syncthreads();  // params of group g landed; previous bwd done with sPhi
-        if (g + 1 < p.ngroups) {
-            if constexpr (PT) {
-                if (tid == 0) tbar_fetch(sTab + (buf ^ 1) * tabsz, p.tab + (size_t)(g + 1) * tabsz, tabsz, &tbar[buf ^ 1]);
-            } else {
-                prefetch_group<C, F, NT>(p, sTap, sTab, g + 1, buf ^ 1, tid);
-            }
-        }
+        if constexpr (!PT)
+            if (g + 1 < p.ngroups) prefetch_group<C, F, NT>(p, sTap, sTab, g + 1, buf ^ 1, tid);
         const float* tapg = PT ? kp + g * F * C::KP : sTap + buf * F * C::KP;
         const float* tabg = sTab + buf * tabsz;
         if constexpr (PT) forward_group_pt<C, MS, RF, F, NT, FAST>(p, sU, sPhi, tapg, tabg, tid);
         else forward_group<C, MS, RF, F, FAST>(p, sU, sPhi, tapg, tabg, tid);
         __syncthreads();
+        // PT: the table is free -- fetch the next group's under fix-up + backward
+        if constexpr (PT)
+            if (tid == 0 && g + 1 < p.ngroups) tbar_fetch(sTab, p.tab3 + (size_t)(g + 1) * tabsz, tabsz, &tbar);
         fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
         if constexpr (PT) backward_group_pt<C, MS, RB, F>(sPhi, tapg, ox0, oy0, force);
         else backward_group<C, MS, RB, F>(sPhi, tapg, split, ox0, oy0, force);
@@ -870,8 +906,8 @@ __device__ __forceinline__ void stage_split_body_pt(const StageArgs& p, const Sp
     extern __shared__ __align__(16) float smem[];
     float* sU = smem;
     float* sPhi = sU + C::SU;
-    float* sTab = sPhi + F * C::SPHI + 2 * F * C::KP;
-    const int tabsz = F * p.tab_stride;
+    float* sTab = sPhi + F * C::SPHI;   // one cubic table buffer
+    const int tabsz = F * p.tab3_stride;
     const int tid = threadIdx.x;
     const int ng = p.ngroups;
     const bool top_halo = p.flags & 0x2u;
@@ -885,16 +921,15 @@ __device__ __forceinline__ void stage_split_body_pt(const StageArgs& p, const Sp
     const int obx = tid % C::OBX, oby = tid / C::OBX;
     const int ox0 = obx * 4, oy0 = oby * RB;
 
-    __shared__ __align__(8) uint64_t tbar[2];
+    __shared__ __align__(8) uint64_t tbar;  // the table buffer's fills
     if (tid == 0) {
-        tbar_init(&tbar[0]);
-        tbar_init(&tbar[1]);
-        if (nunits > 0) tbar_fetch(sTab, p.tab + (size_t)(ubeg % ng) * tabsz, tabsz, &tbar[0]);
+        tbar_init(&tbar);
+        if (nunits > 0) tbar_fetch(sTab, p.tab3 + (size_t)(ubeg % ng) * tabsz, tabsz, &tbar);
     }
-    __syncthreads();  // barriers initialised before anyone waits
+    __syncthreads();  // barrier initialised before anyone waits
     pdl_wait();       // the previous stage wrote u_in
     pdl_trigger();    // the reduction may be scheduled as CTAs retire
-    int k = 0;        // units done (table buffer k & 1, its fill (k >> 1))
+    int k = 0;        // units done (= table fills completed)
     while (k < nunits) {
         const int unit = ubeg + k;
         const int tile = unit / ng, g0 = unit - tile * ng;
@@ -906,18 +941,17 @@ __device__ __forceinline__ void stage_split_body_pt(const StageArgs& p, const Sp
         stage_u_tile<C, NT>(p, sU, p.u_in + (int64_t)img * p.img_stride, Y0, X0, top_halo, bot_halo, tid);
         float* dst = ws.part + (size_t)tile * ng * TPX + oy0 * TW + ox0;
         for (int g = g0; g < gend; ++g, ++k) {
-            const int buf = k & 1;
-            tbar_wait(&tbar[buf], (k >> 1) & 1);
+            tbar_wait(&tbar, k & 1);
             __syncthreads();  // table + u tile in smem; previous unit done with sPhi
-            if (tid == 0 && k + 1 < nunits)
-                tbar_fetch(sTab + (buf ^ 1) * tabsz, p.tab + (size_t)(g + 1 < ng ? g + 1 : 0) * tabsz, tabsz,
-                           &tbar[buf ^ 1]);
             const float* tapg = kp + g * F * C::KP;
-            const float* tabg = sTab + buf * tabsz;
+            const float* tabg = sTab;
             // all RF rows' table lookups before the phi stores (with the taps
             // out of the registers this pays here too: +1% C2 on B200)
             forward_group_pt<C, MS, RF, F, NT, FAST>(p, sU, sPhi, tapg, tabg, tid);
             __syncthreads();
+            // the table is free: fetch the next unit's under fix-up + backward
+            if (tid == 0 && k + 1 < nunits)
+                tbar_fetch(sTab, p.tab3 + (size_t)(g + 1 < ng ? g + 1 : 0) * tabsz, tabsz, &tbar);
             fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
             float force[RB][4];
 #pragma unroll

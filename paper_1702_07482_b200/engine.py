@@ -130,6 +130,11 @@ class DeviceModel:
         # polynomial RBF tables: (max |p - phi| float64 coeffs, fp32 coeffs,
         # max sum|w|, intervals)
         self.rbf_fit = (err.value, e32.value, scale.value, ni.value)
+        # cubic table of the parameter-space-taps kernels: (max |p - phi|
+        # float64 coeffs, fp32 coeffs, intervals; 0 = none)
+        _lib.check(L.tnrd_model_rbf_fit_cubic(h, ctypes.byref(err), ctypes.byref(e32),
+                                              ctypes.byref(ni)))
+        self.rbf_fit_cubic = (err.value, e32.value, ni.value)
         self._plans = {}
         self._plan_lock = threading.Lock()
         self._status = {}

@@ -1,9 +1,10 @@
 """The large-tile CUDA-core kernels read the filter taps either from the
-kernel parameter space (uniform datapath, the default) or from shared
-memory (tnrd_set_param_taps(0)).  The arithmetic is the same FMA chain in
-the same order, so the tile kernel must agree bit for bit; the split kernel
-agrees bit for bit when both use the same filter groups (and to fp32
-summation order otherwise).  Both variants meet the parity bar."""
+kernel parameter space (uniform datapath) with the cubic RBF table (the
+default), or from shared memory with the degree-7 table
+(tnrd_set_param_taps(0)).  The convolutions are the same FMA chains in the
+same order; phi differs by the two interpolants (both at the fp32
+resolution of phi), so the variants agree to ~1e-6 relative and both meet
+the parity bar; each is bit-reproducible."""
 import numpy as np
 import pytest
 
@@ -39,12 +40,14 @@ CASES = [  # (H, W, m, nk, T) -- nk odd / not a multiple of 4 exercises the zero
 
 
 @pytest.mark.parametrize("H,W,m,nk,T", CASES)
-def test_tile_kernel_param_taps_bit_identical(cuda, H, W, m, nk, T):
+def test_tile_kernel_param_taps(cuda, H, W, m, nk, T):
     model = synth.make_model(m, nk, T, 63, seed=H + W + m)
     f = np.random.default_rng(H * W).uniform(0, 300, (H, W)).astype(np.float32)
     a = _despeckle(f, model, True, _lib.KERNEL_LARGE_TILES)
+    a2 = _despeckle(f, model, True, _lib.KERNEL_LARGE_TILES)
     b = _despeckle(f, model, False, _lib.KERNEL_LARGE_TILES)
-    assert np.array_equal(a, b)
+    assert np.array_equal(a, a2)
+    assert np.max(np.abs(a - b) / np.abs(b)) <= 2e-5
 
 
 @pytest.mark.parametrize("H,W,m,nk,T", CASES)
@@ -55,7 +58,7 @@ def test_split_kernel_param_taps(cuda, oracle, H, W, m, nk, T):
     a2 = _despeckle(f, model, True, _lib.KERNEL_SPLIT_LARGE)
     b = _despeckle(f, model, False, _lib.KERNEL_SPLIT_LARGE)
     assert np.array_equal(a, a2)                      # bit-reproducible
-    assert np.max(np.abs(a - b) / np.abs(b)) <= 1e-5  # fp32 summation order at most
+    assert np.max(np.abs(a - b) / np.abs(b)) <= 2e-5  # the two RBF interpolants
     ref = oracle.run_diffusion(f.astype(np.float64), model)
     assert parity_stats(a, ref)["rel"] <= 1e-4
 

@@ -154,6 +154,19 @@ def test_rbf_polynomial_tables_accuracy(cuda, key):
     assert err32 <= 1e-7 * scale, dm.rbf_fit    # ~ fp32 resolution of phi
 
 
+@pytest.mark.parametrize("key", ["c1", "c2", "c5"])
+def test_rbf_cubic_tables_accuracy(cuda, key):
+    """The cubic tables of the parameter-space-taps kernels (10 intervals
+    per centre spacing) interpolate phi_i to the fp32 resolution of phi:
+    below 2e-7 of sum|w| with float64 and with fp32 coefficients."""
+    dm = tn.device_model_for(synth.config_model(synth.CONFIGS[key]))
+    err, err32, ni = dm.rbf_fit_cubic
+    scale = dm.rbf_fit[2]
+    assert ni > 0
+    assert err <= 2e-7 * scale, dm.rbf_fit_cubic
+    assert err32 <= 2e-7 * scale, dm.rbf_fit_cubic
+
+
 def test_direct_rbf_path_parity(cuda, oracle):
     """A bandwidth so narrow that the polynomial table would not fit in
     shared memory selects the direct all-centre RBF path."""

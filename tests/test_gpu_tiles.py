@@ -125,8 +125,9 @@ def test_auto_small_grid_uses_split_and_matches_tile_kernel(cuda):
 def test_fused_dataflow_bit_identical_to_split_stages(cuda, shape):
     """The fused dataflow despeckle (all stages in one launch, tiles of stage
     t+1 started as their neighbourhood of stage t is reduced) sums the same
-    partials in the same order as the per-stage split kernel: bit-identical
-    output, including the projected variant."""
+    partials in the same order as the per-stage split kernel with the
+    shared-memory taps and degree-7 RBF table: bit-identical output,
+    including the projected variant."""
     torch = cuda
     for variant in ("prox", "projected"):
         model = synth.make_model(7, 12, 4, 63, seed=len(shape) * 10 + shape[-1])
@@ -141,8 +142,10 @@ def test_fused_dataflow_bit_identical_to_split_stages(cuda, shape):
             assert _lib.launch_count() == 2          # setup + one dataflow kernel
             fused2 = dm.despeckle(f)
             _lib.set_stage_kernel(_lib.KERNEL_SPLIT_LARGE)
+            _lib.set_param_taps(False)
             split = dm.despeckle(f)
         finally:
+            _lib.set_param_taps(True)
             _lib.set_stage_kernel(_lib.KERNEL_AUTO)
         assert torch.equal(fused, split)
         assert torch.equal(fused, fused2)
