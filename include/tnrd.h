@@ -176,7 +176,7 @@ int tnrd_plan_despeckle_host(tnrd_plan* plan, const float* f_host,
                              float* u_host);
 /* A sequence of `count` host images (each batch*H*W fp32, dense, back to
  * back in f_host / u_host): image i's copies and stages run round-robin on
- * the plan and up to 3 internal twin plans (own streams and buffers; 4 plans
+ * the plan and up to 5 internal twin plans (own streams and buffers; 6 plans
  * for plans of <= 64 MB per buffer, else 2; TNRD_STREAM_DEPTH overrides), so
  * one image's H2D / D2H overlap the next ones' stages and small images run
  * concurrently (pinned host buffers needed for the overlap).  Synchronous; returns the first failing image's

@@ -1732,7 +1732,8 @@ extern "C" int tnrd_plan_despeckle_host_many(tnrd_plan* p, const float* f_host, 
     DeviceGuard dg(p->md->device);
     // pipeline depth: the plan plus depth-1 chained twins, each on its own
     // stream, take the images round-robin.  Measured on B200 (C2 e2e,
-    // MPix/s): depth 1 476, 2 568, 3 600, 4 616; a batch that fills the GPU
+    // MPix/s): depth 1 476, 2 568, 3 600, 4 616 (r01 split kernels); with
+    // the r01 cubic kernels 4 726, 6 763, 8 764.  A batch that fills the GPU
     // by itself gains nothing (C5: 174 / 178 / 179), so deep pipelines are
     // kept to plans of <= 64 MB per buffer.
     static const int depth_env = [] {
@@ -1740,7 +1741,7 @@ extern "C" int tnrd_plan_despeckle_host_many(tnrd_plan* p, const float* f_host, 
         return e ? std::min(std::max(atoi(e), 1), 8) : 0;
     }();
     const size_t plan_bytes = (size_t)p->batch * p->H * p->W * sizeof(float);
-    const int depth = depth_env ? depth_env : (plan_bytes <= (size_t(64) << 20) ? 4 : 2);
+    const int depth = depth_env ? depth_env : (plan_bytes <= (size_t(64) << 20) ? 6 : 2);
     std::vector<tnrd_plan*> ring{p};
     for (int d = 1; d < depth; ++d) {
         tnrd_plan* last = ring.back();
