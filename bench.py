@@ -480,6 +480,16 @@ def main():
     tpath = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(cfg.name)
+    # what the stage kernel executes (ncu --set full SASS counts, committed
+    # under profiles/) at this run's live launch time: the executed FP32
+    # rate, which -- unlike SURVEY's algorithmic count -- cannot exceed peak
+    executed = None
+    epath = os.path.join(REPO, "profiles", "executed.json")
+    if os.path.exists(epath):
+        ex = json.load(open(epath)).get(cfg.name)
+        if ex:
+            ex_tf = 2.0 * ex["ffma_per_px_stage"] * px_launch / (launch_ms * 1e-3) / 1e12
+            executed = dict(ex, achieved_tflops=ex_tf, frac=ex_tf / peak_tf)
     conf = workload_config(cfg, args, B)
     if cfg.name == "c4":
         conf.update({"parallelism": f"row strips x{world}, {cfg.m - 1}-row u halo exchanged per stage (NCCL P2P)",
@@ -498,6 +508,7 @@ def main():
             "work": f"SURVEY 8(d): W_flop={w_flop(cfg)} FLOP/pixel-stage x {px_launch} px per stage",
             "launch_ms": launch_ms,
             "stage_kernels": stage_kernels,
+            "executed": executed,
             "survey_combined": {
                 "unit": "MPix*stages/s", "achieved": ach_pxst, "peak": roof_pxst,
                 "frac": ach_pxst / roof_pxst,
