@@ -71,3 +71,17 @@ def test_c2_auto_param_taps_parity(cuda, oracle):
     ref = oracle.run_diffusion(f.astype(np.float64), model)
     st = parity_stats(u, ref, clean)
     assert st["rel"] <= 1e-4 and st["dpsnr"] <= 0.01, st
+
+
+def test_models_beyond_the_parameter_block_fall_back(cuda, oracle):
+    """m = 7 with 60 filters does not fit the 10 KB TapBlock: the large-tile
+    launches fall back to the shared-memory-taps kernels (same results as
+    forcing them) and still meet the parity bar."""
+    model = synth.make_model(7, 60, 2, 63, seed=11)
+    f = np.random.default_rng(5).uniform(0, 300, (200, 260)).astype(np.float32)
+    for mode in (_lib.KERNEL_LARGE_TILES, _lib.KERNEL_SPLIT_LARGE):
+        a = _despeckle(f, model, True, mode)
+        b = _despeckle(f, model, False, mode)
+        assert np.array_equal(a, b)
+        ref = oracle.run_diffusion(f.astype(np.float64), model)
+        assert parity_stats(a, ref)["rel"] <= 1e-4
