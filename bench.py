@@ -118,6 +118,21 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- CPU baseline
 
+def host_info() -> dict:
+    """CPU model and logical core count of this host (SURVEY 8(d) asks for
+    both beside the CPU baseline)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count()}
+
+
 def cpu_reference_run(cfg, model, f, budget_s: float):
     """Time the float64 C port of the reference algorithm (all host
     threads) on f, shrinking to a centred crop if a run exceeds budget_s.
@@ -175,7 +190,7 @@ def run_reference_arm(args, cfg, rank):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(cfg, args, per_rank_batch=1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads,
-                         "kind": "port", "sample": sample},
+                         "kind": "port", "sample": sample, **host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -526,7 +541,7 @@ def main():
         img0 = f_host[0] if cfg.name != "c4" else f_host[0][:512, :512]
         rate, dt, sample, threads = cpu_reference_run(cfg, model, img0, 20.0)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads,
-                                "kind": "port", "sample": sample}
+                                "kind": "port", "sample": sample, **host_info()}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
