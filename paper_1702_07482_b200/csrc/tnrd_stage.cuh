@@ -982,10 +982,13 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel_split_pt(const StageArg
 // u_in, floored on the first stage exactly as the tile kernels stage it).
 // Up to 24 groups all partial loads of a quad are in flight at once, with
 // the quad's u and f loads.
+#ifndef TNRD_REDUCE_NV
+#define TNRD_REDUCE_NV 24
+#endif
 template <int TH, int TW>
 __global__ void __launch_bounds__(128) stage_reduce_kernel(const StageArgs p, const SplitWs ws) {
     constexpr int TPX = TH * TW;
-    constexpr int NV = 24;
+    constexpr int NV = TNRD_REDUCE_NV;
     const int ng = p.ngroups;
     const int64_t quads = (int64_t)ws.tiles * (TPX / 4);
     bool bad = false;
@@ -1012,19 +1015,22 @@ __global__ void __launch_bounds__(128) stage_reduce_kernel(const StageArgs p, co
             fq[c] = __ldg(fin + off);
         }
         const float* src = ws.part + (size_t)tile * ng * TPX + i;
-        float4 v[NV];
+        // batches of NV partial loads in flight, summed in group order
+        float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        for (int g0 = 0; g0 < ng; g0 += NV) {
+            float4 v[NV];
 #pragma unroll
-        for (int g = 0; g < NV; ++g)
-            if (g < ng) v[g] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)g * TPX));
-        float4 acc = v[0];
+            for (int g = 0; g < NV; ++g)
+                if (g0 + g < ng) v[g] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)(g0 + g) * TPX));
 #pragma unroll
-        for (int g = 1; g < NV; ++g)
-            if (g < ng) {
-                acc.x += v[g].x; acc.y += v[g].y; acc.z += v[g].z; acc.w += v[g].w;
-            }
-        for (int g = NV; g < ng; ++g) {
-            const float4 w = __ldcg(reinterpret_cast<const float4*>(src + (size_t)g * TPX));
-            acc.x += w.x; acc.y += w.y; acc.z += w.z; acc.w += w.w;
+            for (int g = 0; g < NV; ++g)
+                if (g0 + g < ng) {
+                    if (g0 + g == 0) {
+                        acc = v[0];
+                    } else {
+                        acc.x += v[g].x; acc.y += v[g].y; acc.z += v[g].z; acc.w += v[g].w;
+                    }
+                }
         }
         const float fa[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll
