@@ -158,6 +158,25 @@ def cpu_reference_run(cfg, model, f, budget_s: float):
     return side * side / dt / 1e6, dt, sample, threads
 
 
+def single_core_run(cfg, model, f, side: int = 128) -> dict:
+    """SURVEY 8(d)'s 1-core figure: the same C port on one thread over a
+    centred side x side crop (a few seconds)."""
+    from oracle import oracle as O
+    O.build()
+    O.set_threads(1)
+    try:
+        H, W = f.shape
+        y0, x0 = (H - side) // 2, (W - side) // 2
+        crop = f[y0:y0 + side, x0:x0 + side].astype(np.float64)
+        t0 = time.perf_counter()
+        O.run_diffusion(crop, model)
+        dt = time.perf_counter() - t0
+    finally:
+        O.set_threads(-1)
+    return {"value": side * side / dt / 1e6, "unit": UNIT, "cores": 1,
+            "sample": f"{side}x{side} centred crop of image 0, 1 thread"}
+
+
 def run_reference_arm(args, cfg, rank):
     if rank != 0:
         return
@@ -541,7 +560,8 @@ def main():
         img0 = f_host[0] if cfg.name != "c4" else f_host[0][:512, :512]
         rate, dt, sample, threads = cpu_reference_run(cfg, model, img0, 20.0)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads,
-                                "kind": "port", "sample": sample, **host_info()}
+                                "kind": "port", "sample": sample, **host_info(),
+                                "single_core": single_core_run(cfg, model, img0)}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
