@@ -526,6 +526,9 @@ extern "C" int tnrd_status_decode(const uint32_t* h, int* bad_stage) {
 #ifndef TNRD_PT_RF
 #define TNRD_PT_RF 5
 #endif
+#ifndef TNRD_PT_SPLIT_RF
+#define TNRD_PT_SPLIT_RF TNRD_PT_RF
+#endif
 #ifndef TNRD_PT_M9_RF
 #define TNRD_PT_M9_RF 2
 #endif
@@ -571,7 +574,16 @@ struct LargeTile { static constexpr int TH = 64, TW = 64, RF = TNRD_LARGE_RF, RB
 #endif
 // split kernel units: one filter per unit halves the granularity of the SM
 // balance (a 512^2 image = 64 tiles x 48 units over 148 SMs)
-struct SplitTile { static constexpr int TH = 64, TW = 64, RF = TNRD_LARGE_RF, RB = 4, NT = 256, F = TNRD_SPLIT_F; };
+#ifndef TNRD_SPLIT_TH
+#define TNRD_SPLIT_TH 64
+#endif
+#ifndef TNRD_SPLIT_RB
+#define TNRD_SPLIT_RB 4
+#endif
+struct SplitTile {
+    static constexpr int TH = TNRD_SPLIT_TH, TW = 64, RF = TNRD_LARGE_RF, RB = TNRD_SPLIT_RB, NT = 256,
+                         F = TNRD_SPLIT_F;
+};
 
 
 constexpr size_t kMaxSplitBytes = size_t(1) << 30;
@@ -714,7 +726,8 @@ struct StageKernel {
 
     // parameter-space taps (TapBlock, tnrd_stage.cuh): large tiles only (one
     // thread per output block, so the tap address is warp-uniform)
-    static constexpr bool kPT = T::TH == 64 && FAST;
+    // one thread per output block (no filter split: warp-uniform filter)
+    static constexpr bool kPT = (T::TW / 4) * (T::TH / T::RB) == T::NT && FAST;
     using TB = TapBlock<MS <= 7 ? 2560 : kMaxParamTaps>;
     // forward blocking (measured on B200): m = 7 RF = 5 (252 blocks per
     // filter for 256 threads); m = 9 RF = 2 (C5 172.5 MPix/s; RF = 3 167.4,
@@ -723,7 +736,8 @@ struct StageKernel {
     static constexpr int F_TILE_PT = TNRD_PT_TILE_F;
     using CPT = StageCfg<MS, TH, TW, RF_PT, RB, NT, F_TILE_PT>;
     static constexpr int F_SPLIT_PT = TNRD_PT_SPLIT_F;
-    using CPS = StageCfg<MS, TH, TW, RF_PT, RB, NT, F_SPLIT_PT>;
+    static constexpr int RF_SPLIT_PT = MS >= 9 ? TNRD_PT_M9_RF : TNRD_PT_SPLIT_RF;
+    using CPS = StageCfg<MS, TH, TW, RF_SPLIT_PT, RB, NT, F_SPLIT_PT>;
     // filters per split unit (the parameter-space kernel has its own)
     static int split_f(const StageArgs& a) { return pt_fits(a) ? F_SPLIT_PT : F; }
     // htaps: this stage's taps on the host, [nk_pad][kp]
@@ -849,7 +863,7 @@ struct StageKernel {
                 static std::mutex mu;
                 static uint64_t attr_set = 0;
                 static int occ[64] = {0};
-                auto kern = stage_kernel_split_pt<MS, TH, TW, RF_PT, RB, NT, FAST, F_SPLIT_PT, TNRD_PT_MINB, TB>;
+                auto kern = stage_kernel_split_pt<MS, TH, TW, RF_SPLIT_PT, RB, NT, FAST, F_SPLIT_PT, TNRD_PT_MINB, TB>;
                 TB tb;
                 fill_taps(tb, htaps, a.nk);
                 return launch_split_k(kern, pt_smem<CPS, F_SPLIT_PT>(a), F_SPLIT_PT, a, batch, wsp, s, mu,
