@@ -1938,8 +1938,14 @@ extern "C" int tnrd_stage_backward(const tnrd_model* md, int t, const float* u_p
         }
         CUDA_TRY(cudaGetLastError());
         if (grad_k || grad_w) {
-            const size_t rsm = sizeof(float) * (2 * (size_t)m * (train::kSeg + 2 * (m / 2)) + 4 * train::kSeg);
-            train::bwd_reduce_kernel<<<dim3((unsigned)nblk, (unsigned)a.nf), 256, rsm, s>>>(a, nseg);
+            const size_t rsm = sizeof(float) * (2 * (size_t)m * train::red_row_stride(m) + 4 * train::kSeg);
+            const dim3 rgrid((unsigned)nblk, (unsigned)a.nf);
+            switch (m) {
+                case 3: train::bwd_reduce_kernel<3><<<rgrid, 256, rsm, s>>>(a, nseg); break;
+                case 5: train::bwd_reduce_kernel<5><<<rgrid, 256, rsm, s>>>(a, nseg); break;
+                case 7: train::bwd_reduce_kernel<7><<<rgrid, 256, rsm, s>>>(a, nseg); break;
+                default: train::bwd_reduce_kernel<9><<<rgrid, 256, rsm, s>>>(a, nseg); break;
+            }
             const int tot = a.nf * nout;
             train::bwd_final_kernel<<<(tot + 3) / 4, 128, 0, s>>>(part, outd, a.nf, nblk, nout);
             CUDA_TRY(cudaGetLastError());

@@ -353,32 +353,48 @@ __device__ __forceinline__ float warp_sum(float s) {
     return s;
 }
 
+// staged rows of bwd_reduce_kernel: logical column c at c + c / 8, so the
+// 8-column windows of the 32 lanes start 9 floats apart (distinct banks)
+__host__ __device__ constexpr int red_row_stride(int m) { return kSeg + 2 * (m / 2) + (kSeg + 2 * (m / 2)) / 8 + 1; }
+__device__ __forceinline__ int pad8(int c) { return c + (c >> 3); }
+
+// Parameter partials of one (image row, 256-column segment, filter): the
+// m^2 kernel-gradient terms sum_x u[a][x + b] w1[x] and sum_x phi[a][x + b]
+// g_t[x] as one work item per (term, tap row a) -- each lane owns 8
+// consecutive columns, loads the row window once and keeps the m sums of
+// that row in registers, then one xor tree per output -- and the M
+// RBF-design terms sum_x G_j(z[x]) v[x], one item per output; items are
+// dealt round-robin to the warps.  Fixed order throughout: bit-reproducible.
+template <int MS>
 __global__ void __launch_bounds__(256) bwd_reduce_kernel(const BwdArgs a, int nseg) {
     extern __shared__ float sm[];
+    constexpr int R = MS / 2, MM = MS * MS;
+    constexpr int SW = kSeg + 2 * R;           // staged row width
+    constexpr int SWP = red_row_stride(MS);    // padded row stride
+    static_assert(kSeg == 32 * 8, "one 8-column window per lane");
     const int n = a.H * a.W;
     const int fi = blockIdx.y;
     const int y = blockIdx.x / nseg, seg = blockIdx.x % nseg;
     const int x0 = seg * kSeg, nx = min(kSeg, a.W - x0);
-    const int m = a.m, mm = m * m, r = m / 2, nout = 2 * mm + a.s.M;
-    const int SW = kSeg + 2 * r;               // staged row width
-    float* su = sm;                            // [m][SW]
-    float* sp = su + m * SW;                   // [m][SW]
-    float* sw1 = sp + m * SW;                  // [kSeg] each
+    const int nout = 2 * MM + a.s.M;
+    float* su = sm;                            // [MS][SWP]
+    float* sp = su + MS * SWP;                 // [MS][SWP]
+    float* sw1 = sp + MS * SWP;                // [kSeg] each
     float* sgt = sw1 + kSeg;
     float* sz = sgt + kSeg;
     float* sv = sz + kSeg;
     const size_t fo = (size_t)fi * n;
-    for (int t = threadIdx.x; t < m * SW; t += blockDim.x) {
+    for (int t = threadIdx.x; t < MS * SW; t += blockDim.x) {
         const int aa = t / SW, c = t % SW;
-        const int xx = x0 + c - r;
+        const int xx = x0 + c - R;
         float uv = 0.0f, pv = 0.0f;
-        if (c < nx + 2 * r) {
-            const size_t off = (size_t)mir1(y + aa - r, a.H) * a.W + mir1(xx, a.W);
+        if (c < nx + 2 * R) {
+            const size_t off = (size_t)mir1(y + aa - R, a.H) * a.W + mir1(xx, a.W);
             uv = __ldg(a.u + off);
             pv = __ldg(a.phi + fo + off);
         }
-        su[t] = uv;
-        sp[t] = pv;
+        su[aa * SWP + pad8(c)] = uv;
+        sp[aa * SWP + pad8(c)] = pv;
     }
     for (int t = threadIdx.x; t < kSeg; t += blockDim.x) {
         const bool ok = t < nx;
@@ -390,23 +406,42 @@ __global__ void __launch_bounds__(256) bwd_reduce_kernel(const BwdArgs a, int ns
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int o = warp; o < nout; o += nw) {
-        float s = 0.0f;
-        if (o < 2 * mm) {
-            const bool second = o >= mm;
-            const int oo = second ? o - mm : o;
-            const float* row = (second ? sp : su) + (oo / m) * SW + (oo % m);
-            const float* adj = second ? sgt : sw1;
-            for (int x = lane; x < nx; x += 32) s = fmaf(row[x], adj[x], s);
+    double* part = a.part + ((size_t)fi * a.nblk + blockIdx.x) * nout;
+    // work items: (term, tap row) pairs -- 8-column windows, MS sums each --
+    // then the M RBF-design outputs, dealt round-robin to the warps
+    const int nitems = 2 * MS + a.s.M;
+    for (int it = warp; it < nitems; it += nw) {
+        if (it < 2 * MS) {
+            const int term = it / MS, aa = it - term * MS;
+            const float* row = (term == 0 ? su : sp) + aa * SWP;
+            const float* adj = term == 0 ? sw1 : sgt;   // zero beyond nx
+            float w[8], v[8 + 2 * R], acc[MS];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) w[k] = adj[8 * lane + k];
+#pragma unroll
+            for (int j = 0; j < 8 + 2 * R; ++j) v[j] = row[pad8(8 * lane + j)];
+#pragma unroll
+            for (int b = 0; b < MS; ++b) {
+                acc[b] = 0.0f;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc[b] = fmaf(v[k + b], w[k], acc[b]);
+            }
+#pragma unroll
+            for (int b = 0; b < MS; ++b) {
+                const float s = warp_sum(acc[b]);
+                if (lane == 0) part[term * MM + aa * MS + b] = s;
+            }
         } else {
-            const float mu = fmaf((float)(o - 2 * mm), a.s.delta, a.s.mu0);
+            const int o = 2 * MM + (it - 2 * MS);
+            const float mu = fmaf((float)(o - 2 * MM), a.s.delta, a.s.mu0);
+            float s = 0.0f;
             for (int x = lane; x < nx; x += 32) {
                 const float d = sz[x] - mu;
                 s = fmaf(ex2f(d * d * a.s.cE), sv[x], s);
             }
+            s = warp_sum(s);
+            if (lane == 0) part[o] = s;
         }
-        s = warp_sum(s);
-        if (lane == 0) a.part[((size_t)fi * a.nblk + blockIdx.x) * nout + o] = s;
     }
 }
 
