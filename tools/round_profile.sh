@@ -21,15 +21,18 @@ ncu --set full --import-source on --clock-control none -k regex:stage_kernel -s 
     -o $O/c3_tile python tools/prof_one.py c3 256 > $O/ncu_c3.log 2>&1
 ncu --set full --clock-control none -k regex:stage_kernel -s 2 -c 1 \
     -o $O/c4_tile python tools/prof_one.py c4 1 > $O/ncu_c4.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:stage_kernel -s 2 -c 1 \
+    -o $O/c5_tile python tools/prof_one.py c5 32 > $O/ncu_c5.log 2>&1
+python tools/parity_probe.py > $O/parity_probe.txt 2>&1
 # summaries on the box (gpurun brings back <= 64 MiB): keep the split
 # kernel's report, text for the rest
-PX_C3=$((256*512*512)); PX_C2=$((512*512)); PX_C4=$((16384*16384))
-for r in c2_split:$PX_C2 c2_reduce:$PX_C2 c3_tile:$PX_C3 c4_tile:$PX_C4; do
+PX_C3=$((256*512*512)); PX_C2=$((512*512)); PX_C4=$((16384*16384)); PX_C5=$((32*1024*1024))
+for r in c2_split:$PX_C2 c2_reduce:$PX_C2 c3_tile:$PX_C3 c4_tile:$PX_C4 c5_tile:$PX_C5; do
     n=${r%%:*}; px=${r#*:}
     python tools/ncu_summary.py $O/$n.ncu-rep > $O/ncu_summary_$n.txt 2>&1
     python tools/ncu_sass_stats.py $O/$n.ncu-rep $px >> $O/ncu_summary_$n.txt 2>&1
     ncu -i $O/$n.ncu-rep --page details --csv > $O/ncu_details_$n.csv 2>/dev/null
 done
 python tools/launch_times.py $O/launches_c2.csv > $O/launch_times_c2.txt 2>&1
-rm -f $O/c2_reduce.ncu-rep $O/c3_tile.ncu-rep $O/c4_tile.ncu-rep
+rm -f $O/c2_reduce.ncu-rep $O/c3_tile.ncu-rep $O/c4_tile.ncu-rep $O/c5_tile.ncu-rep
 ls -la $O
