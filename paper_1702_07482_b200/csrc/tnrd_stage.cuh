@@ -20,6 +20,10 @@
 //     polynomial table (float64 Chebyshev fit on the host, error ~1e-9 of
 //     sum|w|): 2 conflict-free LDS.128 + 7 FFMA per response instead of
 //     M=63 exponentials;
+//   * the large-tile default kernels (stage_kernel_pt / _split_pt, DESIGN.md
+//     4.9-4.10) instead read the taps from the kernel parameter space
+//     (uniform datapath) and phi from a cubic table (one LDS.128 + 3 FFMA)
+//     fetched per filter group with cp.async.bulk on an mbarrier;
 //   * phi halos that fall outside the image are filled by mirroring the
 //     in-image phi values (reference pads phi itself, diffusion.py:180);
 //   * backward pass: each thread owns an RB x 4 output block for half of
