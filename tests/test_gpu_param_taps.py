@@ -85,3 +85,25 @@ def test_models_beyond_the_parameter_block_fall_back(cuda, oracle):
         assert np.array_equal(a, b)
         ref = oracle.run_diffusion(f.astype(np.float64), model)
         assert parity_stats(a, ref)["rel"] <= 1e-4
+
+
+@pytest.mark.parametrize("mode", [_lib.KERNEL_LARGE_TILES, _lib.KERNEL_SPLIT_LARGE], ids=["tile", "split"])
+def test_padded_row_stride_matches_contiguous(cuda, mode):
+    """Row stride ld > W and image stride > ld * H (views into wider, taller
+    buffers) give the same bits as the dense layout."""
+    torch = cuda
+    model = synth.make_model(7, 10, 2, 63, seed=4)
+    B, H, W = 2, 150, 181
+    f = np.random.default_rng(9).uniform(0, 300, (B, H, W)).astype(np.float32)
+    dm = tn.device_model_for(model)
+    _lib.set_stage_kernel(mode)
+    try:
+        dense = dm.despeckle(torch.from_numpy(f).cuda())
+        big = [torch.zeros(B, H + 5, W + 13, device="cuda") for _ in range(3)]
+        fv, ov, wv = (b[:, :H, :W] for b in big)
+        fv.copy_(torch.from_numpy(f).cuda())
+        got = dm.despeckle(fv, out=ov, work=wv)
+    finally:
+        _lib.set_stage_kernel(_lib.KERNEL_AUTO)
+    assert got.stride() == ov.stride() and got.stride(-2) == W + 13
+    assert torch.equal(got.contiguous(), dense)
