@@ -61,7 +61,16 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if SHARED_GPU:
+        local = 0
     return rank, world, local
+
+
+# Functional check of the N > 1 code path on a one-GPU box: every rank on
+# cuda:0, gloo for the barriers and the max-over-ranks reductions.  Not a
+# measurement (ranks share the SMs); the line says so.  C4's strip exchange
+# needs NCCL and is not supported in this mode.
+SHARED_GPU = os.environ.get("TNRD_BENCH_SHARED_GPU") == "1"
 
 
 # ---------------------------------------------------------------- clocks
@@ -278,7 +287,11 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARED_GPU:
+            assert cfg.name != "c4", "TNRD_BENCH_SHARED_GPU: C4 strips need NCCL"
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_1702_07482_b200 as tn
     from paper_1702_07482_b200 import _lib, strips
@@ -287,6 +300,7 @@ def main():
     model = synth.config_model(cfg)
     dm = tn.device_model_for(model)
     dev = torch.device("cuda", local)
+    red_dev = torch.device("cpu") if SHARED_GPU else dev   # max-over-ranks reductions
     stream = torch.cuda.Stream(dev)
     status = tn.engine.Status(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -396,7 +410,7 @@ def main():
                     for k in range(args.steps) for t in range(cfg.T)]
         launch_ms = sum(stage_ms) / len(stage_ms)
     if dist is not None:
-        tt = torch.tensor([ms, launch_ms], device=dev, dtype=torch.float64)
+        tt = torch.tensor([ms, launch_ms], device=red_dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms, launch_ms = tt.tolist()
     total_px = world * px_rank if cfg.name != "c4" else H * W
@@ -488,7 +502,7 @@ def main():
         for k in range(e2e_steps):
             assert np.array_equal(seq_u[k].numpy(), ref_u), "e2e result differs"
     if dist is not None:
-        tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        tt = torch.tensor([e2e_ms], device=red_dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = tt.item()
 
@@ -556,6 +570,9 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clk,
     }
+    if SHARED_GPU:
+        line["not_a_measurement"] = (f"TNRD_BENCH_SHARED_GPU: {world} ranks shared cuda:0 "
+                                     "(functional check of the N>1 path)")
     if world == 1 and not args.no_cpu_baseline:
         img0 = f_host[0] if cfg.name != "c4" else f_host[0][:512, :512]
         rate, dt, sample, threads = cpu_reference_run(cfg, model, img0, 20.0)

@@ -1,0 +1,16 @@
+#!/bin/bash
+# Functional check of bench.py's N > 1 path (torchrun, barriers, max-over-
+# ranks reductions, per-rank shards) on a ONE-GPU box: TNRD_BENCH_SHARED_GPU=1
+# puts every rank on cuda:0 with gloo.  The lines are marked
+# not_a_measurement; the N-GPU numbers come from the driver's scaling run.
+# Usage (under gpurun): bash tools/shared_gpu_check.sh
+mkdir -p gpurun_out/r01_nproc
+O=gpurun_out/r01_nproc
+export TNRD_BENCH_SHARED_GPU=1
+P=29500
+for spec in "2 c2" "2 c3" "2 c5" "8 c2" "8 c3" "8 c5"; do
+  set -- $spec; P=$((P+1))
+  timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node $1 --master-addr 127.0.0.1 --master-port $P \
+     bench.py --gpus $1 --workload $2 --steps 3 --warmup 3 > $O/n$1_$2.json 2> $O/n$1_$2.err
+  echo "n$1 $2 EXIT $?" >> $O/summary.txt
+done
