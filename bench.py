@@ -354,6 +354,19 @@ def main():
         def step(evs=None):
             # T fused stage launches through the C ABI; final stage lands in `out`
             L.tnrd_status_reset(sptr, sh)
+            if B >= 2:
+                # batches: one tnrd_despeckle call, which may run the two
+                # halves' stage chains on two streams (DESIGN.md §7b item 5);
+                # events bracket the whole step, per-stage time = step / T
+                if evs is not None:
+                    evs[0].record(stream)
+                _lib.check(L.tnrd_despeckle(dm.handle, ctypes.c_void_p(f.data_ptr()),
+                                            ctypes.c_void_p(out.data_ptr()),
+                                            ctypes.c_void_p(work.data_ptr()),
+                                            B, H, W, W, H * W, sptr, sh))
+                if evs is not None:
+                    evs[cfg.T].record(stream)
+                return
             cur = f
             for t in range(cfg.T):
                 dst = out if (cfg.T - 1 - t) % 2 == 0 else work
@@ -401,9 +414,9 @@ def main():
 
     step_ms = [evs[k][0].elapsed_time(evs[k][cfg.T]) for k in range(args.steps)]
     ms = sum(step_ms) / len(step_ms)
-    if cfg.name == "c4":
-        # stage launches interleave with halo exchanges: per-launch time is
-        # taken from the exchange-free N=1 pattern (step / T) for the roofline
+    if cfg.name == "c4" or px_rank > H * W:
+        # C4: stage launches interleave with halo exchanges; batches: one
+        # tnrd_despeckle call per step -- per-launch time = step / T
         launch_ms = ms / cfg.T
     else:
         stage_ms = [evs[k][t].elapsed_time(evs[k][t + 1])

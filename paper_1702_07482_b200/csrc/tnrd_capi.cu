@@ -119,6 +119,10 @@ struct tnrd_model {
     mutable std::map<cudaStream_t, SplitBuf> fws;
     // z-field planes (tnrd_stage_zf.cuh), one per stream
     mutable std::map<cudaStream_t, SplitBuf> zws;
+    // batch fork (tnrd_despeckle): per caller stream, a second stream and
+    // the fork / join events (DESIGN.md §7b item 5)
+    struct ForkRes { cudaStream_t s2 = nullptr; cudaEvent_t fork = nullptr, join = nullptr; };
+    mutable std::map<cudaStream_t, ForkRes> forks;
 };
 
 // 0 = auto (the faster kernel as measured on B200: currently
@@ -447,6 +451,12 @@ extern "C" int tnrd_model_destroy(tnrd_model* md) {
         for (auto& kv : md->ws) cudaFree(kv.second.ptr);
         for (auto& kv : md->zws) cudaFree(kv.second.ptr);
         for (auto& kv : md->fws) cudaFree(kv.second.ptr);
+        for (auto& kv : md->forks) {
+            cudaStreamSynchronize(kv.second.s2);
+            cudaStreamDestroy(kv.second.s2);
+            cudaEventDestroy(kv.second.fork);
+            cudaEventDestroy(kv.second.join);
+        }
     }
     delete md;
     return TNRD_OK;
@@ -1455,6 +1465,56 @@ static int despeckle_fused(const tnrd_model* md, const float* f, float* u_out, f
     return md->fast ? despeckle_fused_m<true>(md, st, batch, s) : despeckle_fused_m<false>(md, st, batch, s);
 }
 
+static int despeckle_stages(const tnrd_model* md, const float* f, float* u_out, float* work,
+                            int batch, int H, int W, int64_t ld, int64_t image_stride,
+                            uint32_t* d_status, cudaStream_t s) {
+    const float* cur = f;
+    for (int t = 0; t < md->T; ++t) {
+        float* dst = ((md->T - 1 - t) % 2 == 0) ? u_out : work;
+        const uint32_t fl = t == 0 ? (TNRD_STAGE_FLOOR_INPUT | TNRD_STAGE_CHECK_F) : 0u;
+        int rc = launch_stage(md, t, cur, f, dst, batch, H, W, ld, image_stride, fl, d_status, s);
+        if (rc) return rc;
+        cur = dst;
+    }
+    return TNRD_OK;
+}
+
+// Batch fork (DESIGN.md §7b item 5, measured with tools/multistream_probe.py):
+// in auto mode, when even the smaller half of the batch selects the
+// large-tile kernel (>= 3 waves), run the halves on two streams.  Returns the
+// fork resources of caller stream s, or nullptr for one stream.
+// TNRD_BATCH_FORK=0 turns it off (A/B runs).
+static const tnrd_model::ForkRes* batch_fork(const tnrd_model* md, int batch, int H, int W,
+                                             cudaStream_t s) {
+    static const bool enabled = [] {
+        const char* e = std::getenv("TNRD_BATCH_FORK");
+        return !(e && e[0] == '0');
+    }();
+    if (!enabled || batch < 2 || g_kernel_mode.load() != 0) return nullptr;
+    StageArgs a = stage_args(md, 0, 0u);
+    a.H = H; a.W = W;
+    if (cc_variant(a, batch / 2) != 1) return nullptr;
+    std::lock_guard<std::mutex> lk(md->ws_mu);
+    auto& fr = md->forks[s];
+    if (!fr.s2) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+            return nullptr;   // resources are created outside any capture
+        int prio = 0;
+        cudaStreamGetPriority(s, &prio);
+        if (cudaStreamCreateWithPriority(&fr.s2, cudaStreamNonBlocking, prio) != cudaSuccess ||
+            cudaEventCreateWithFlags(&fr.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&fr.join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            if (fr.s2) cudaStreamDestroy(fr.s2);
+            if (fr.fork) cudaEventDestroy(fr.fork);
+            md->forks.erase(s);
+            return nullptr;
+        }
+    }
+    return &fr;
+}
+
 extern "C" int tnrd_despeckle(const tnrd_model* md, const float* f, float* u_out, float* work,
                               int batch, int H, int W, int64_t ld, int64_t image_stride,
                               uint32_t* d_status, void* stream) {
@@ -1467,15 +1527,24 @@ extern "C" int tnrd_despeckle(const tnrd_model* md, const float* f, float* u_out
     cudaStream_t s = (cudaStream_t)stream;
     rc = despeckle_fused(md, f, u_out, work, batch, H, W, ld, image_stride, d_status, s);
     if (rc != -1) return rc;   // ran (or failed) as one fused launch
-    const float* cur = f;
-    for (int t = 0; t < md->T; ++t) {
-        float* dst = ((md->T - 1 - t) % 2 == 0) ? u_out : work;
-        const uint32_t fl = t == 0 ? (TNRD_STAGE_FLOOR_INPUT | TNRD_STAGE_CHECK_F) : 0u;
-        rc = launch_stage(md, t, cur, f, dst, batch, H, W, ld, image_stride, fl, d_status, s);
-        if (rc) return rc;
-        cur = dst;
-    }
-    return TNRD_OK;
+    const tnrd_model::ForkRes* fr = batch_fork(md, batch, H, W, s);
+    if (!fr) return despeckle_stages(md, f, u_out, work, batch, H, W, ld, image_stride, d_status, s);
+    // images are independent: the two halves' stage chains run on two
+    // streams, so one half's stage t + 1 fills the SMs the other's last tile
+    // wave of stage t leaves idle.  Same kernel for both halves and the
+    // whole batch, so the same bits.  Capture-safe (event fork / join).
+    const int b0 = (batch + 1) / 2;
+    const int64_t off = (int64_t)b0 * image_stride;
+    CUDA_TRY(cudaEventRecord(fr->fork, s));
+    CUDA_TRY(cudaStreamWaitEvent(fr->s2, fr->fork, 0));
+    rc = despeckle_stages(md, f, u_out, work, b0, H, W, ld, image_stride, d_status, s);
+    if (rc == TNRD_OK)
+        rc = despeckle_stages(md, f + off, u_out + off, work ? work + off : nullptr, batch - b0, H, W,
+                              ld, image_stride, d_status, fr->s2);
+    // join even after a failed launch, so a capture on s stays well formed
+    CUDA_TRY(cudaEventRecord(fr->join, fr->s2));
+    CUDA_TRY(cudaStreamWaitEvent(s, fr->join, 0));
+    return rc;
 }
 
 // ----------------------------------------------------------------- plans
