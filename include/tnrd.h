@@ -154,7 +154,11 @@ int tnrd_stage(const tnrd_model* model, int t, const float* u_in,
 
 /* All T stages, ping-ponging between u_out and work (same shape), the
  * final stage landing in u_out.  Stage 0 reads f as u_0 with the 1e-6 floor
- * (initial_state) and validates f into the status block. */
+ * (initial_state) and validates f into the status block.  Large batches
+ * may run their two halves on an internal second stream forked from and
+ * joined back into `stream` (same bits; ordering on `stream` is kept, and
+ * the call may be captured into a CUDA graph after one eager call on that
+ * stream); TNRD_BATCH_FORK=0 in the environment disables it. */
 int tnrd_despeckle(const tnrd_model* model, const float* f, float* u_out,
                    float* work, int batch, int H, int W, int64_t ld,
                    int64_t image_stride, uint32_t* d_status, void* stream);
