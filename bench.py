@@ -527,8 +527,18 @@ def main():
     # ---- roofline of the fused stage (SURVEY 8(d) algorithmic work); small
     # grids run it as the split kernel + its ordered reduction (2 launches)
     stage_kernels = int(round(launches / (args.steps * cfg.T)))
-    stage_kernels = {1: "stage_kernel (fused tile kernel)",
-                     2: "stage_kernel_split + stage_reduce_kernel"}.get(stage_kernels, str(stage_kernels))
+    # batch fork (tnrd_despeckle, DESIGN.md 7b item 5): the half batch still
+    # has >= 3 waves of 64x64 tiles at 2 CTAs per SM -> two tile-kernel
+    # launches per stage, one per half, on two streams
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    half_tiles = -(-H // 64) * -(-W // 64) * (px_rank // (H * W) // 2)
+    forked = (cfg.name != "c4" and px_rank > H * W and half_tiles >= 3 * 2 * sms
+              and os.environ.get("TNRD_BATCH_FORK", "1")[:1] != "0")
+    if forked and stage_kernels == 2:
+        stage_kernels = "stage_kernel (fused tile kernel) x 2 batch halves on two streams"
+    else:
+        stage_kernels = {1: "stage_kernel (fused tile kernel)",
+                         2: "stage_kernel_split + stage_reduce_kernel"}.get(stage_kernels, str(stage_kernels))
     px_launch = px_rank
     flop_launch = w_flop(cfg) * px_launch
     achieved_tf = flop_launch / (launch_ms * 1e-3) / 1e12
