@@ -1,25 +1,30 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 TNRD despeckling path (contract: see DESIGN.md §Bench).
+"""Benchmark of the B200 TNRD despeckling path (contract: DESIGN.md §5).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c5]
-                    [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W]
+                    [--workload c1|c2|c3|c4|c5] [--impl ours|reference]
 
 A step = one full despeckle (T fused stages) of one batch of the workload.
-Default workload = BASELINE.json configs[1] (C2: one 512x512 image, 7x7,
-Nk=48, T=5).  Under torchrun each rank despeckles its own image(s) (C2:
-weak scaling, one image per rank; C3/C5: the batch split over ranks,
-strong scaling); no data-path collective.  Rank 0 prints ONE JSON line.
+Default workload = C3 (BASELINE.json configs[2]): 256 images of 512x512,
+7x7, Nk=48, T=5 -- the batch the metric quotes "at 1/2/4/8 B200", sharded
+over the ranks (strong scaling, no data-path collective).  C4 splits one
+16384^2 scene into row strips with a per-stage halo exchange (NCCL P2P);
+C1/C2 are single images (replicas, one per rank); C5 is the 9x9 / Nk=80 /
+T=8 batch.  Under torchrun every rank despeckles its shard; rank 0 prints
+ONE JSON line.  At N > 1 the line carries `verify`: every rank's per-image
+(per-strip) output hashes against rank 0's N = 1 recomputation of the whole
+workload after the timed region.
 
 --impl reference times the reference's CPU algorithm: the reference is pure
 Python/numpy and cannot travel to the GPU box, so the float64 C port in
-oracle/ (pinned bit-for-bit-ish to the reference's golden vectors, see
-tests/test_oracle.py) runs with every host thread on a bounded sample of
-the same workload.
+oracle/ (pinned to the reference's golden vectors, tests/test_oracle.py)
+runs with every host thread on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
 import argparse
 import ctypes
+import hashlib
 import json
 import os
 import statistics
@@ -35,10 +40,19 @@ sys.path.insert(0, REPO)
 METRIC = ("megapixels/sec for full TNRD despeckle (7×7, 48 filters, "
           "5 stages) at 1/2/4/8 B200")
 UNIT = "MPix/s"
+DEFAULT_WORKLOAD = "c3"
+DEFAULT_STEPS = {"c1": 200, "c2": 200, "c3": 20, "c4": 5, "c5": 10}
+
+
+def w_contraction(cfg) -> int:
+    """FLOP per pixel-stage of the two 49x48 contractions the direct method
+    cannot skip: forward filter bank + adjoint, Nk m^2 FMA each (FMA = 2)."""
+    return 4 * cfg.nk * cfg.m * cfg.m
 
 
 def w_flop(cfg) -> int:
-    """algorithmic FLOP per pixel-stage (FMA = 2)."""
+    """algorithmic FLOP per pixel-stage (FMA = 2), charging
+    M = 63 Gaussian terms per response."""
     return 4 * cfg.nk * cfg.m * cfg.m + 5 * cfg.nk * cfg.M + 10
 
 
@@ -49,12 +63,23 @@ def w_sfu(cfg) -> int:
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--_cpu-worker", dest="cpu_worker", default=None, help=argparse.SUPPRESS)
+    a = ap.parse_args()
+    if a.steps is None:
+        a.steps = DEFAULT_STEPS[a.workload]
+    return a
+
+
+# Functional check of the N > 1 code path on a one-GPU box: every rank on
+# cuda:0, gloo for the barriers, reductions and C4's (host-staged) halo
+# exchange.  Not a measurement (ranks share the SMs); the line says so.
+SHARED_GPU = os.environ.get("TNRD_BENCH_SHARED_GPU") == "1"
 
 
 def dist_env():
@@ -64,13 +89,6 @@ def dist_env():
     if SHARED_GPU:
         local = 0
     return rank, world, local
-
-
-# Functional check of the N > 1 code path on a one-GPU box: every rank on
-# cuda:0, gloo for the barriers and the max-over-ranks reductions.  Not a
-# measurement (ranks share the SMs); the line says so.  C4's strip exchange
-# needs NCCL and is not supported in this mode.
-SHARED_GPU = os.environ.get("TNRD_BENCH_SHARED_GPU") == "1"
 
 
 # ---------------------------------------------------------------- clocks
@@ -126,10 +144,11 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU baseline
+# The reference's algorithm on the host cores: the float64 C port in oracle/
+# (test infrastructure; used here only as the reported baseline).
 
 def host_info() -> dict:
-    """CPU model and logical core count of this host (SURVEY 8(d) asks for
-    both beside the CPU baseline)."""
+    """CPU model, logical cores and RAM of this host."""
     model = "unknown"
     try:
         with open("/proc/cpuinfo") as fh:
@@ -139,51 +158,119 @@ def host_info() -> dict:
                     break
     except OSError:
         pass
-    return {"cpu_model": model, "os_cpu_count": os.cpu_count()}
+    ram = None
+    try:
+        ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2 ** 30
+    except (ValueError, OSError):
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(),
+            "ram_gib": round(ram, 1) if ram else None}
 
 
-def cpu_reference_run(cfg, model, f, budget_s: float):
-    """Time the float64 C port of the reference algorithm (all host
-    threads) on f, shrinking to a centred crop if a run exceeds budget_s.
-    Returns (mpix_per_s, seconds, sample_desc, threads)."""
+def _crop(cfg, index: int, side: int) -> np.ndarray:
+    """A centred side x side crop of workload image `index` (C4: of the
+    scene's first tile row), float64."""
+    from paper_1702_07482_b200 import synth
+    if cfg.tiled:
+        y0 = (1024 - side) // 2 + 1024 * (index % 16)
+        x0 = (1024 - side) // 2 + 1024 * ((index // 16) % 16)
+        return synth.scene_crop(cfg, y0, y0 + side, x0, x0 + side).astype(np.float64)
+    _, f = synth.noisy_image(cfg, index % cfg.batch)
+    y0, x0 = (cfg.H - side) // 2, (cfg.W - side) // 2
+    return f[y0:y0 + side, x0:x0 + side].astype(np.float64)
+
+
+def cpu_worker(spec: str) -> None:
+    """Subprocess body (--_cpu-worker JSON): run the C port on one crop and
+    print {seconds, t_end, peak_rss_mb}; `start` = a wall-clock time to wait
+    for (so P workers start together)."""
+    import resource
+    a = json.loads(spec)
+    from oracle import oracle as O
+    from paper_1702_07482_b200 import synth
+    cfg = synth.CONFIGS[a["workload"]]
+    model = synth.config_model(cfg)
+    crop = _crop(cfg, a["index"], a["side"])
+    O.build()
+    O.set_threads(a["threads"])
+    while time.time() < a.get("start", 0):
+        time.sleep(0.001)
+    t0 = time.perf_counter()
+    O.run_diffusion(crop, model)
+    dt = time.perf_counter() - t0
+    print(json.dumps({"seconds": dt, "t_end": time.time(),
+                      "peak_rss_mb": resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1024.0}))
+
+
+def _spawn_worker(workload, index, side, threads, start=0.0):
+    spec = json.dumps({"workload": workload, "index": index, "side": side,
+                       "threads": threads, "start": start})
+    return subprocess.Popen([sys.executable, os.path.join(REPO, "bench.py"), "--_cpu-worker", spec],
+                            stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, cwd=REPO)
+
+
+def _collect(p):
+    out, err = p.communicate()
+    if p.returncode != 0:
+        raise RuntimeError(f"cpu worker failed: {err[-500:]}")
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def cpu_all_threads(cfg, budget_s: float):
+    """The C port with every host thread on image 0 of the workload (a
+    centred crop, shrunk until one run fits budget_s).  Returns (MPix/s,
+    seconds, side, threads, peak_rss_mb)."""
     from oracle import oracle as O
     O.build()
     O.set_threads(-1)
     threads = O.threads()
-    H, W = f.shape
-    side = min(H, W)
+    side = min(cfg.H, cfg.W, 1024)
     while True:
-        y0, x0 = (H - side) // 2, (W - side) // 2
-        crop = f[y0:y0 + side, x0:x0 + side].astype(np.float64)
-        t0 = time.perf_counter()
-        O.run_diffusion(crop, model)
-        dt = time.perf_counter() - t0
-        if dt <= budget_s or side <= 64:
+        r = _collect(_spawn_worker(cfg.name, 0, side, -1))
+        if r["seconds"] <= budget_s or side <= 64:
             break
-        side = max(64, int(side * (budget_s / dt) ** 0.5 * 0.9) // 8 * 8)
-    sample = (f"{side}x{side} crop of image 0 ({'full image' if side == min(H, W) and H == W else 'bounded sample'}), "
-              f"{cfg.m}x{cfg.m}, Nk={cfg.nk}, T={cfg.T}, float64 C port of the reference "
-              f"algorithm (oracle/tnrd_oracle.c), {threads} threads")
-    return side * side / dt / 1e6, dt, sample, threads
+        side = max(64, int(side * (budget_s / r["seconds"]) ** 0.5 * 0.9) // 8 * 8)
+    return side * side / r["seconds"] / 1e6, r["seconds"], side, threads, r["peak_rss_mb"]
 
 
-def single_core_run(cfg, model, f, side: int = 128) -> dict:
-    """SURVEY 8(d)'s 1-core figure: the same C port on one thread over a
-    centred side x side crop (a few seconds)."""
-    from oracle import oracle as O
-    O.build()
-    O.set_threads(1)
-    try:
-        H, W = f.shape
-        y0, x0 = (H - side) // 2, (W - side) // 2
-        crop = f[y0:y0 + side, x0:x0 + side].astype(np.float64)
-        t0 = time.perf_counter()
-        O.run_diffusion(crop, model)
-        dt = time.perf_counter() - t0
-    finally:
-        O.set_threads(-1)
-    return {"value": side * side / dt / 1e6, "unit": UNIT, "cores": 1,
-            "sample": f"{side}x{side} centred crop of image 0, 1 thread"}
+def cpu_baseline(cfg) -> dict:
+    """SURVEY 8(d)'s CPU figures for the line: all host threads on one image
+    (the value), one core (extrapolated to a full image), P single-threaded
+    processes on P different images at once (image-parallel throughput),
+    and peak RSS."""
+    info = host_info()
+    rate, dt, side, threads, rss = cpu_all_threads(cfg, 20.0)
+    full = side == min(cfg.H, cfg.W) and cfg.H == cfg.W and not cfg.tiled
+    out = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+           "sample": (f"{side}x{side} {'(full image)' if full else 'centred crop'} of image 0, "
+                      f"{cfg.m}x{cfg.m}, Nk={cfg.nk}, T={cfg.T}, float64 C port of the reference "
+                      f"algorithm (oracle/tnrd_oracle.c), {threads} threads"),
+           "peak_rss_mb": round(rss, 1), **info}
+    # one core: a small crop, extrapolated per pixel-stage to one full image
+    cs = 128 if cfg.m <= 7 else 96
+    r1 = _collect(_spawn_worker(cfg.name, 0, cs, 1))
+    per_px = r1["seconds"] / (cs * cs)
+    out["single_core"] = {
+        "value": cs * cs / r1["seconds"] / 1e6, "unit": UNIT, "cores": 1,
+        "sample": f"{cs}x{cs} centred crop of image 0, 1 thread",
+        "full_image_seconds_extrapolated": per_px * cfg.H * cfg.W,
+        "note": f"extrapolated per pixel from the {cs}x{cs} crop to one {cfg.H}x{cfg.W} image",
+        "peak_rss_mb": round(r1["peak_rss_mb"], 1)}
+    # P processes x 1 thread, each on its own image (the reference's natural
+    # parallelism: images are independent, SPEC.md:255)
+    P = os.cpu_count() or 1
+    start = time.time() + 1.5
+    procs = [_spawn_worker(cfg.name, i, cs, 1, start) for i in range(P)]
+    res = [_collect(p) for p in procs]
+    wall = max(r["t_end"] for r in res) - start
+    out["image_parallel"] = {
+        "value": P * cs * cs / wall / 1e6, "unit": UNIT, "processes": P, "cores": P,
+        "sample": f"{P} processes x 1 thread, each a {cs}x{cs} crop of its own image, started together",
+        "peak_rss_mb_per_process": round(max(r["peak_rss_mb"] for r in res), 1),
+        "note": ("the reference's numpy path materialises the (Nk,H,W,M) RBF design tensor: "
+                 "SURVEY 8(d) measured ~6.4 GB RSS per 512^2 image for C2/C3 (~42 GB for C5), "
+                 "which caps P at RAM/RSS for the reference itself; the C port streams it")}
+    return out
 
 
 def run_reference_arm(args, cfg, rank):
@@ -191,17 +278,11 @@ def run_reference_arm(args, cfg, rank):
         return
     from paper_1702_07482_b200 import synth
     model = synth.config_model(cfg)
-    if cfg.tiled:
-        f = synth.scene_crop(cfg, 0, 1024, 0, 1024)
-    else:
-        _, f = synth.noisy_image(cfg, 0)
     per_step = max(2.0, 150.0 / max(1, args.steps + args.warmup))
-    rate, dt, sample, threads = cpu_reference_run(cfg, model, f, per_step)
+    rate, dt, side, threads, rss = cpu_all_threads(cfg, per_step)
     from oracle import oracle as O
-    side = int(round((rate * 1e6 * dt) ** 0.5))
-    y0 = (f.shape[0] - side) // 2
-    x0 = (f.shape[1] - side) // 2
-    crop = f[y0:y0 + side, x0:x0 + side].astype(np.float64)
+    O.set_threads(-1)
+    crop = _crop(cfg, 0, side)
     for _ in range(max(0, args.warmup - 1)):
         O.run_diffusion(crop, model)
     times = []
@@ -211,6 +292,9 @@ def run_reference_arm(args, cfg, rank):
         times.append(time.perf_counter() - t0)
     ms = 1e3 * sum(times) / len(times)
     value = side * side / (ms * 1e3)
+    sample = (f"{side}x{side} centred crop of image 0 per step, {cfg.m}x{cfg.m}, Nk={cfg.nk}, "
+              f"T={cfg.T}, float64 C port of the reference algorithm (oracle/tnrd_oracle.c), "
+              f"{threads} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -218,7 +302,8 @@ def run_reference_arm(args, cfg, rank):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(cfg, args, per_rank_batch=1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads,
-                         "kind": "port", "sample": sample, **host_info()},
+                         "kind": "port", "sample": sample, "peak_rss_mb": round(rss, 1),
+                         **host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -259,28 +344,50 @@ def measure_peaks(torch, L, stream):
     return out
 
 
-def setup_images(cfg, rank, world):
+def shard_indices(cfg, rank, world):
     if cfg.batch == 1:
-        idx = [rank]                      # C2: one image per rank (weak)
-    else:
-        per = cfg.batch // world          # C3/C5: batch sharded (strong)
-        idx = list(range(rank * per, (rank + 1) * per))
-    return idx, np.stack([synth_mod().noisy_image(cfg, i)[1] for i in idx])
+        return [rank]                     # C1/C2: one image per rank (replicas)
+    per = cfg.batch // world              # C3/C5: batch sharded (strong)
+    return list(range(rank * per, (rank + 1) * per))
 
 
-def synth_mod():
-    from paper_1702_07482_b200 import synth
-    return synth
+def img_hash(a: np.ndarray) -> str:
+    return hashlib.sha1(np.ascontiguousarray(a, dtype=np.float32).tobytes()).hexdigest()[:16]
+
+
+def stamp_ok(entry) -> tuple[bool, str]:
+    """executed.json entries are stamped with the hash of the sources the
+    profiled library was built from (__graft_entry__.source_hash)."""
+    import __graft_entry__ as ge
+    cur = ge.source_hash()
+    got = entry.get("source_hash")
+    if got == cur:
+        return True, cur
+    return False, f"stale: profiled build {got}, this build {cur}"
 
 
 def main():
     args = parse()
+    if args.cpu_worker is not None:
+        cpu_worker(args.cpu_worker)
+        return
     rank, world, local = dist_env()
-    synth = synth_mod()
+    from paper_1702_07482_b200 import synth
     cfg = synth.CONFIGS[args.workload]
     if args.impl == "reference":
         run_reference_arm(args, cfg, rank)
         return
+
+    # inputs first (host cores, before any CUDA work in this process)
+    if cfg.name == "c4":
+        from paper_1702_07482_b200 import strips
+        lay = strips.StripLayout(cfg.H, cfg.W, world, rank, halo=cfg.m - 1)
+        r0, r1 = lay.rows
+        f_host = synth.scene_rows_parallel(cfg, r0, r1)[None]
+        idx = None
+    else:
+        idx = shard_indices(cfg, rank, world)
+        f_host = synth.noisy_batch(cfg, idx)
 
     import torch
     torch.cuda.set_device(local)
@@ -288,7 +395,6 @@ def main():
     if world > 1:
         import torch.distributed as dist
         if SHARED_GPU:
-            assert cfg.name != "c4", "TNRD_BENCH_SHARED_GPU: C4 strips need NCCL"
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -309,16 +415,17 @@ def main():
     sptr = ctypes.c_void_p(status.buf.data_ptr())
 
     if cfg.name == "c4":
-        # one scene split into row strips, per-stage halo exchange (NCCL P2P)
-        lay = strips.StripLayout(H, W, world, rank, halo=cfg.m - 1)
-        r0, r1 = lay.rows
+        # one scene split into row strips, per-stage halo exchange (NCCL P2P;
+        # host-staged gloo when the ranks share one GPU)
         h, n = lay.halo, lay.n
-        f_host = synth.scene_rows(cfg, r0, r1)[None]
         f_ext = torch.zeros(n + 2 * h, W, dtype=torch.float32, device=dev)
         f_ext[h:h + n] = torch.from_numpy(f_host[0]).to(dev)
         bufs = [torch.empty_like(f_ext), torch.empty_like(f_ext)]
         stage_fn = strips.gpu_stage_fn(dm, status=status, stream=stream)
-        exch = strips.exchange_halos if world > 1 else (lambda *a, **k: None)
+        if world == 1:
+            exch = lambda *a, **k: None  # noqa: E731
+        else:
+            exch = strips.exchange_halos_host if SHARED_GPU else strips.exchange_halos
         B, px_rank = 1, n * W
         result = {}
 
@@ -344,7 +451,6 @@ def main():
         def final_output():
             return result["u"][h:h + n]
     else:
-        idx, f_host = setup_images(cfg, rank, world)
         B = len(idx)
         f = torch.from_numpy(f_host).to(dev)
         out = torch.empty_like(f)
@@ -411,6 +517,7 @@ def main():
             dist.barrier()
         clk = clocks.stop()
         status.check()
+        out_host = final_output().cpu().numpy()
 
     step_ms = [evs[k][0].elapsed_time(evs[k][cfg.T]) for k in range(args.steps)]
     ms = sum(step_ms) / len(step_ms)
@@ -430,6 +537,7 @@ def main():
     value = total_px / (ms * 1e3)          # MPix/s, all ranks
 
     # ---- e2e: HOST buffers in, HOST result out, copies inside the timed region
+    e2e_steps, e2e_same = 0, None
     if cfg.name == "c4" and world == 1:
         # the whole scene through tnrd_plan_despeckle_host (C ABI): row bands
         # on their own streams, each band's H2D / stages / D2H ordered by
@@ -454,6 +562,7 @@ def main():
         e1.record(pstream)
         e1.synchronize()
         e2e_ms = e0.elapsed_time(e1) / e2e_steps
+        e2e_same = bool(np.array_equal(pin_u.numpy(), out_host))
         e2e_path = ("tnrd_plan_despeckle_host (C ABI), one scene per step: row bands with "
                     "event-ordered H2D / stages / D2H on their own streams, pinned host buffers")
     elif cfg.name == "c4":
@@ -475,20 +584,15 @@ def main():
             e1.record(stream)
             e1.synchronize()
         e2e_ms = e0.elapsed_time(e1) / e2e_steps
-        e2e_path = "strip H2D + run_strip (NCCL halo exchange, fused stages) + D2H + status check"
+        e2e_path = "strip H2D + run_strip (halo exchange, fused stages) + D2H + status check"
     else:
-        pin_f = torch.from_numpy(f_host).pin_memory()
-        pin_u = torch.empty_like(pin_f).pin_memory()
         plan = dm._plan(B, H, W)
         pstream = torch.cuda.ExternalStream(L.tnrd_plan_stream(plan), device=dev)
-        for _ in range(3):
-            _lib.check(L.tnrd_plan_despeckle_host(plan, ctypes.c_void_p(pin_f.data_ptr()),
-                                                  ctypes.c_void_p(pin_u.data_ptr())))
+        per_img = int(f_host.nbytes)
         # a stream of steps through tnrd_plan_despeckle_host_many: every step
         # still copies its input in and its result out (pinned buffers), and
         # one step's copies overlap the next step's stages
-        per_img = int(f_host.nbytes)
-        e2e_steps = max(3, min(args.steps, 50, max(2, (1 << 30) // per_img)))
+        e2e_steps = max(3, min(args.steps, 50, max(2, (768 << 20) // per_img)))
         seq_f = torch.empty((e2e_steps,) + tuple(f_host.shape), dtype=torch.float32).pin_memory()
         seq_f.copy_(torch.from_numpy(f_host).unsqueeze(0).expand_as(seq_f))
         seq_u = torch.empty_like(seq_f).pin_memory()
@@ -511,38 +615,90 @@ def main():
         e2e_ms = e0.elapsed_time(e1) / e2e_steps
         e2e_path = ("tnrd_plan_despeckle_host_many (C ABI): a stream of steps, each with its "
                     "H2D + T stages + D2H + status read, pinned host buffers")
-        ref_u = final_output().cpu().numpy()
-        for k in range(e2e_steps):
-            assert np.array_equal(seq_u[k].numpy(), ref_u), "e2e result differs"
+        e2e_same = all(bool(np.array_equal(seq_u[k].numpy(), out_host)) for k in range(e2e_steps))
+        del seq_f, seq_u
     if dist is not None:
         tt = torch.tensor([e2e_ms], device=red_dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = tt.item()
+
+    # ---- N > 1: every rank's output against rank 0's N = 1 recomputation
+    verify = None
+    if dist is not None and not args.no_verify:
+        if cfg.name == "c4":
+            mine = [(r0, r1, img_hash(out_host))]
+        else:
+            mine = [(i, img_hash(out_host[j])) for j, i in enumerate(idx)]
+        got = [None] * world
+        dist.all_gather_object(got, mine)
+        if rank == 0:
+            t0 = time.perf_counter()
+            if cfg.name == "c4":
+                whole = synth.scene_rows_parallel(cfg, 0, H)
+                u1 = dm.despeckle(torch.from_numpy(whole).to(dev)).cpu().numpy()
+                items = [x for part in got for x in part]
+                bad_items = [(a, b) for a, b, hsh in items if img_hash(u1[a:b]) != hsh]
+                what = f"{len(items)} strips"
+            else:
+                all_idx = [x[0] for part in got for x in part]
+                fb = torch.from_numpy(synth.noisy_batch(cfg, all_idx)).to(dev)
+                if cfg.batch == 1:
+                    u1 = np.stack([dm.despeckle(fb[j]).cpu().numpy() for j in range(len(all_idx))])
+                else:
+                    u1 = dm.despeckle(fb).cpu().numpy()
+                ref = {i: img_hash(u1[j]) for j, i in enumerate(all_idx)}
+                items = [x for part in got for x in part]
+                bad_items = [i for i, hsh in items if ref[i] != hsh]
+                what = f"{len(items)} images"
+            verify = {"ok": not bad_items, "checked": what, "mismatches": bad_items[:8],
+                      "how": ("sha1 of each rank's fp32 output (per image / per strip) vs rank 0 "
+                              "recomputing the whole workload in one N=1 call after the timed region"),
+                      "seconds": round(time.perf_counter() - t0, 2)}
+        dist.barrier()
+
+    # ---- latency: one image through a fresh one-image plan, host to host
+    latency = None
+    if rank == 0:
+        lat_img = f_host[0]
+        pin_f1 = torch.from_numpy(np.ascontiguousarray(lat_img)).pin_memory()
+        pin_u1 = torch.empty_like(pin_f1).pin_memory()
+        plan1 = dm._plan(1, lat_img.shape[0], lat_img.shape[1])
+        lat = []
+        reps = 3 if lat_img.size > (1 << 22) else 20
+        for k in range(reps + 2):
+            t0 = time.perf_counter()
+            _lib.check(L.tnrd_plan_despeckle_host(plan1, ctypes.c_void_p(pin_f1.data_ptr()),
+                                                  ctypes.c_void_p(pin_u1.data_ptr())))
+            if k >= 2:
+                lat.append(time.perf_counter() - t0)
+        lms = 1e3 * statistics.median(lat)
+        latency = {"ms": lms, "value": lat_img.size / (lms * 1e3), "unit": UNIT,
+                   "image": f"{lat_img.shape[0]}x{lat_img.shape[1]}",
+                   "path": ("tnrd_plan_despeckle_host (C ABI), one image, one plan, pinned host "
+                            "buffers, no overlap: host wall clock around H2D + T stages + D2H + "
+                            f"status read, median of {reps}")}
 
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the fused stage (SURVEY 8(d) algorithmic work); small
-    # grids run it as the split kernel + its ordered reduction (2 launches)
+    # ---- roofline of the dominant kernel (the fused stage)
     stage_kernels = int(round(launches / (args.steps * cfg.T)))
-    # batch fork (tnrd_despeckle, DESIGN.md 7b item 5): the half batch still
-    # has >= 3 waves of 64x64 tiles at 2 CTAs per SM -> two tile-kernel
-    # launches per stage, one per half, on two streams
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     half_tiles = -(-H // 64) * -(-W // 64) * (px_rank // (H * W) // 2)
     forked = (cfg.name != "c4" and px_rank > H * W and half_tiles >= 3 * 2 * sms
               and os.environ.get("TNRD_BATCH_FORK", "1")[:1] != "0")
     if forked and stage_kernels == 2:
-        stage_kernels = "stage_kernel (fused tile kernel) x 2 batch halves on two streams"
+        stage_kernels = "stage_kernel_pt (fused tile kernel) x 2 batch halves on two streams"
     else:
-        stage_kernels = {1: "stage_kernel (fused tile kernel)",
-                         2: "stage_kernel_split + stage_reduce_kernel"}.get(stage_kernels, str(stage_kernels))
+        stage_kernels = {1: "stage_kernel_pt (fused tile kernel)",
+                         2: "stage_kernel_split_pt + stage_reduce_kernel"}.get(stage_kernels,
+                                                                                 str(stage_kernels))
     px_launch = px_rank
-    flop_launch = w_flop(cfg) * px_launch
-    achieved_tf = flop_launch / (launch_ms * 1e-3) / 1e12
     peak_tf = peaks["fp32_tflops"]
+    contraction_tf = w_contraction(cfg) * px_launch / (launch_ms * 1e-3) / 1e12
+    alg_tf = w_flop(cfg) * px_launch / (launch_ms * 1e-3) / 1e12
     peak_sfu = peaks["mufu_ex2_gops"] * 1e9
     t_roof = max(w_flop(cfg) / (peak_tf * 1e12), w_sfu(cfg) / peak_sfu)  # s per pixel-stage
     roof_pxst = 1.0 / t_roof / 1e6                                        # MPix*stages/s
@@ -551,19 +707,22 @@ def main():
     tpath = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(cfg.name)
-    # what the stage kernel executes (ncu --set full SASS counts, committed
-    # under profiles/) at this run's live launch time: the executed FP32
-    # rate, which -- unlike SURVEY's algorithmic count -- cannot exceed peak
-    executed = None
+    # what the stage kernel executes (ncu --set full SASS counts of THIS
+    # build, profiles/executed.json, stamped with the source hash) at this
+    # run's live launch time
+    executed, executed_frac = None, None
     epath = os.path.join(REPO, "profiles", "executed.json")
     if os.path.exists(epath):
         ex = json.load(open(epath)).get(cfg.name)
         if ex:
+            ok, why = stamp_ok(ex)
             ex_tf = 2.0 * ex["ffma_per_px_stage"] * px_launch / (launch_ms * 1e-3) / 1e12
-            executed = dict(ex, achieved_tflops=ex_tf, frac=ex_tf / peak_tf)
+            executed = dict(ex, achieved_tflops=ex_tf, stamp=why if not ok else "current build")
+            executed_frac = ex_tf / peak_tf if ok else None
     conf = workload_config(cfg, args, B)
     if cfg.name == "c4":
-        conf.update({"parallelism": f"row strips x{world}, {cfg.m - 1}-row u halo exchanged per stage (NCCL P2P)",
+        conf.update({"parallelism": (f"row strips x{world}, {cfg.m - 1}-row u halo exchanged per "
+                                     f"stage ({'gloo host-staged' if SHARED_GPU else 'NCCL P2P'})"),
                      "rows_per_rank": px_rank // W})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -573,38 +732,49 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": conf,
         "roofline": {
-            "bound": "fp32", "unit": "TFLOP/s", "achieved": achieved_tf,
-            "peak": peak_tf, "frac": achieved_tf / peak_tf, "traffic": traffic,
-            "peak_source": "measured on this GPU by tnrd_probe (FFMA); MEASURED_PEAKS.json has no FP32/MUFU entry",
-            "work": f"SURVEY 8(d): W_flop={w_flop(cfg)} FLOP/pixel-stage x {px_launch} px per stage",
+            "bound": "fp32", "unit": "TFLOP/s", "achieved": contraction_tf,
+            "peak": peak_tf, "frac": contraction_tf / peak_tf, "traffic": traffic,
+            "peak_source": "FFMA measured on this GPU by tnrd_probe; MEASURED_PEAKS.json has no FP32 entry",
+            "work": (f"contraction FLOP the direct method cannot skip: 4*Nk*m^2 = {w_contraction(cfg)} "
+                     f"per pixel-stage (forward + adjoint {cfg.m}x{cfg.m}x{cfg.nk} FMA) x {px_launch} "
+                     "px per stage launch"),
             "launch_ms": launch_ms,
             "stage_kernels": stage_kernels,
+            "executed_frac": executed_frac,
             "executed": executed,
-            "survey_combined": {
-                "unit": "MPix*stages/s", "achieved": ach_pxst, "peak": roof_pxst,
-                "frac": ach_pxst / roof_pxst,
-                "rule": "t_roof = max(W_flop/P_fp32, W_sfu/P_mufu) with on-box P_fp32, P_mufu",
-                "p_mufu_gops": peaks["mufu_ex2_gops"]},
+            "algorithmic_frac": alg_tf / peak_tf,
+            "algorithmic": {
+                "note": (">1 by construction: SURVEY 8(d)'s W_flop charges 5*Nk*M FLOP of Gaussian "
+                         "terms per pixel-stage, which the tabulated (cubic-interpolated) phi never "
+                         "executes"),
+                "w_flop": w_flop(cfg), "achieved_tflops": alg_tf,
+                "survey_combined": {
+                    "unit": "MPix*stages/s", "achieved": ach_pxst, "peak": roof_pxst,
+                    "frac": ach_pxst / roof_pxst,
+                    "rule": "t_roof = max(W_flop/P_fp32, W_sfu/P_mufu) with on-box P_fp32, P_mufu",
+                    "p_mufu_gops": peaks["mufu_ex2_gops"]}},
         },
         "e2e": {"value": total_px / (e2e_ms * 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": int(f_host.nbytes),
                 "d2h_bytes_per_step": int(f_host.nbytes) + 8,
-                "path": e2e_path},
+                "steps": e2e_steps, "path": e2e_path,
+                "same_bits_as_device_run": e2e_same},
+        "e2e_latency": latency,
         "gpu_launches": int(launches),
         "clocks": clk,
     }
+    if verify is not None:
+        line["verify"] = verify
     if SHARED_GPU:
         line["not_a_measurement"] = (f"TNRD_BENCH_SHARED_GPU: {world} ranks shared cuda:0 "
                                      "(functional check of the N>1 path)")
     if world == 1 and not args.no_cpu_baseline:
-        img0 = f_host[0] if cfg.name != "c4" else f_host[0][:512, :512]
-        rate, dt, sample, threads = cpu_reference_run(cfg, model, img0, 20.0)
-        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads,
-                                "kind": "port", "sample": sample, **host_info(),
-                                "single_core": single_core_run(cfg, model, img0)}
+        line["cpu_baseline"] = cpu_baseline(cfg)
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+    if verify is not None and not verify["ok"]:
+        sys.exit(3)
 
 
 if __name__ == "__main__":

@@ -159,6 +159,15 @@ int tnrd_stage(const tnrd_model* model, int t, const float* u_in,
  * joined back into `stream` (same bits; ordering on `stream` is kept, and
  * the call may be captured into a CUDA graph after one eager call on that
  * stream); TNRD_BATCH_FORK=0 in the environment disables it. */
+/* tnrd_stage that also writes the stage's force (sum_i rot180(k_i) *
+ * phi_i(k_i * u), diffusion.py:171-181) to force_out (same layout as u_out)
+ * in the same launch: diffusion_step's u_next and its trace's
+ * u~ = u - force without a second pass (CUDA-core kernels; not with
+ * TNRD_STAGE_FORCE). */
+int tnrd_stage_force(const tnrd_model* model, int t, const float* u_in,
+                     const float* f, float* u_out, float* force_out, int batch,
+                     int H, int W, int64_t ld, int64_t image_stride,
+                     uint32_t flags, uint32_t* d_status, void* stream);
 int tnrd_despeckle(const tnrd_model* model, const float* f, float* u_out,
                    float* work, int batch, int H, int W, int64_t ld,
                    int64_t image_stride, uint32_t* d_status, void* stream);
@@ -246,6 +255,12 @@ int tnrd_prox_idiv(const float* u_tilde, const float* f, float* out,
 /* Number of kernel launches issued by this library (process-wide) since
  * the last reset (instrumentation for bench.py's gpu_launches). */
 uint64_t tnrd_launch_count(void);
+/* Build features of this library: TNRD_FEATURE_EXPERIMENTS = the opt-in
+ * tensor-core / dataflow stage kernels (modes 2, 5, 8, 9 of
+ * tnrd_set_stage_kernel) are compiled in (-DTNRD_EXPERIMENTS; they are not
+ * in the default build). */
+#define TNRD_FEATURE_EXPERIMENTS 0x1u
+uint32_t tnrd_build_features(void);
 void tnrd_launch_count_reset(void);
 
 /* Peak probes for the roofline denominators (not on the reference's path):

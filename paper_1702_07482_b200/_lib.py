@@ -62,6 +62,8 @@ SIGNATURES = {
                                     ctypes.POINTER(_c_int)]),
     "tnrd_stage": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _c_int, _c_int,
                             _c_int, _c_i64, _c_i64, _c_u32, _vp, _vp]),
+    "tnrd_stage_force": (_c_int, [_vp, _c_int, _vp, _vp, _vp, _vp, _c_int, _c_int,
+                                  _c_int, _c_i64, _c_i64, _c_u32, _vp, _vp]),
     "tnrd_despeckle": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int,
                                 _c_i64, _c_i64, _vp, _vp]),
     "tnrd_plan_create": (_c_int, [_vp, _c_int, _c_int, _c_int,
@@ -86,6 +88,7 @@ SIGNATURES = {
     "tnrd_philox4x32_10": (None, [ctypes.POINTER(_c_u32), ctypes.POINTER(_c_u32),
                                   ctypes.POINTER(_c_u32)]),
     "tnrd_launch_count": (ctypes.c_uint64, []),
+    "tnrd_build_features": (_c_u32, []),
     "tnrd_launch_count_reset": (None, []),
     "tnrd_probe": (_c_int, [_c_int, _c_int, _c_int, _vp,
                             ctypes.POINTER(ctypes.c_double)]),
@@ -163,6 +166,15 @@ def set_param_taps(on: bool) -> None:
     """Large-tile CUDA-core kernels: taps from the kernel parameter space
     (True, default) or staged in shared memory (False); same bits."""
     check(load().tnrd_set_param_taps(int(bool(on))))
+
+
+FEATURE_EXPERIMENTS = 0x1
+
+
+def has_experiments() -> bool:
+    """True if the opt-in tensor-core / dataflow kernels are compiled in
+    (-DTNRD_EXPERIMENTS, tools/build_experiments.sh)."""
+    return bool(load().tnrd_build_features() & FEATURE_EXPERIMENTS)
 
 
 def launch_count() -> int:

@@ -23,14 +23,22 @@
 
 #include "../../include/tnrd.h"
 #include "tnrd_stage.cuh"
+#include "tnrd_speckle.cuh"
+#include "tnrd_train.cuh"
+// The tensor-core and dataflow stage kernels measured slower than the
+// CUDA-core kernels and are built only with
+// -DTNRD_EXPERIMENTS (tools/build_experiments.sh); the shipped library
+// reports TNRD_EUNSUPPORTED for their modes.
+#ifdef TNRD_EXPERIMENTS
 #include "tnrd_stage_tc.cuh"
 #include "tnrd_stage_tc3.cuh"
 #include "tnrd_stage_zf.cuh"
-#include "tnrd_speckle.cuh"
 #include "tnrd_stage_fused.cuh"
-#include "tnrd_train.cuh"
+#endif
 
 using namespace tnrd;
+
+constexpr int kNkPad = 16;   // filters are padded to a multiple of 16 (zero filters)
 
 // ----------------------------------------------------------------- errors
 
@@ -70,6 +78,13 @@ struct DeviceGuard {
 extern "C" const char* tnrd_last_error(void) { return g_err.c_str(); }
 extern "C" const char* tnrd_version(void) { return "tnrd-b200 0.1.0 sm_100a"; }
 extern "C" uint64_t tnrd_launch_count(void) { return g_launches.load(); }
+extern "C" uint32_t tnrd_build_features(void) {
+#ifdef TNRD_EXPERIMENTS
+    return TNRD_FEATURE_EXPERIMENTS;
+#else
+    return 0u;
+#endif
+}
 extern "C" void tnrd_launch_count_reset(void) { g_launches.store(0); }
 
 // ----------------------------------------------------------------- model
@@ -113,6 +128,10 @@ struct tnrd_model {
     // kernels at once); nothing in them outlives a stage
     struct SplitBuf { void* ptr = nullptr; size_t bytes = 0; std::vector<long> key; };
     mutable std::mutex ws_mu;
+    // workspaces outgrown by a larger request: a CUDA graph captured
+    // earlier may still reference them, so they are freed only with the
+    // model (never while a captured launch could replay into them)
+    mutable std::vector<void*> retired;
     mutable std::map<cudaStream_t, SplitBuf> ws;
     // fused dataflow workspaces (counters | stage args | claim sequence |
     // partials), one per stream, rebuilt when the grid geometry changes
@@ -149,7 +168,7 @@ extern "C" int tnrd_set_stage_kernel(int mode) {
 }
 
 // round-to-nearest (ties away) to tf32, as cvt.rna.tf32.f32
-static float tf32_rna_host(float x) {
+[[maybe_unused]] static float tf32_rna_host(float x) {
     uint32_t b;
     std::memcpy(&b, &x, 4);
     b = (b + 0x1000u) & 0xFFFFE000u;
@@ -254,7 +273,7 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
 
     auto* md = new tnrd_model();
     md->m = m; md->nk = nk; md->T = T; md->M = M; md->device = device;
-    md->nk_pad = round_up(nk, tc::kG);  // zero filters beyond nk
+    md->nk_pad = round_up(nk, kNkPad);  // zero filters beyond nk
     md->mu0 = mu0; md->delta = delta; md->gamma = gamma;
     md->lam.assign(lam, lam + T);
     md->kp = round_up(m * m, 4);
@@ -330,9 +349,10 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
             md->fit_err3_32 = std::max(md->fit_err3_32, e3_32[id]);
         }
     }
+    std::vector<float> bop, zop;
+#ifdef TNRD_EXPERIMENTS
     // forward GEMM operand for the tensor-core kernel (kf = rot180(k), split
     // into tf32 hi + lo, K-major), see tnrd_stage_tc.cuh
-    std::vector<float> bop;
     {
         const int ks = (m + 7) / 8, G = md->nk_pad / tc::kG;
         const size_t bo = 2 * tc::kG * 4;                       // floats per (a, kk, prec)
@@ -358,7 +378,6 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
     }
     // z-field forward operand: kf = rot180(k) split into 3 tf32 pieces
     // (hi, mid, lo), K-major [kc][n][4] per (tap row a, K-step, piece)
-    std::vector<float> zop;
     if (m <= 7 && md->nk_pad <= 128) {
         const int ks = (m + 7) / 8, np = md->nk_pad;
         const size_t bo = 2 * (size_t)np * 4;
@@ -383,6 +402,7 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
                                 }
                             }
     }
+#endif
     {
         DeviceGuard dg(device);
         if (!zop.empty()) {
@@ -448,6 +468,8 @@ extern "C" int tnrd_model_destroy(tnrd_model* md) {
         cudaFree(md->d_tab3);
         cudaFree(md->d_bop);
         cudaFree(md->d_zop);
+        cudaDeviceSynchronize();   // retired workspaces may back queued graph replays
+        for (void* q : md->retired) cudaFree(q);
         for (auto& kv : md->ws) cudaFree(kv.second.ptr);
         for (auto& kv : md->zws) cudaFree(kv.second.ptr);
         for (auto& kv : md->fws) cudaFree(kv.second.ptr);
@@ -599,6 +621,7 @@ struct SplitTile {
 constexpr size_t kMaxSplitBytes = size_t(1) << 30;
 static int sm_count();
 
+#ifdef TNRD_EXPERIMENTS
 // ---- fused dataflow despeckle (tnrd_stage_fused.cuh) ----------------------
 
 constexpr int kMaxFusedStages = 8;
@@ -670,8 +693,7 @@ static int fused_workspace(const tnrd_model* md, cudaStream_t s, const std::vect
             return fail(TNRD_ECUDA, "fused workspace must be built before stream capture");
         const std::vector<int> seq = fused_sequence(T, tiles, tiles_x, ng, grid);
         const FusedLayout L = fused_layout(T, tiles, ng, tpx, (int)seq.size());
-        CUDA_TRY(cudaStreamSynchronize(s));
-        if (b.ptr) cudaFree(b.ptr);
+        if (b.ptr) md->retired.push_back(b.ptr);   // a captured graph may still use it
         b.ptr = nullptr;
         b.bytes = 0;
         b.key.clear();
@@ -689,6 +711,8 @@ static int fused_workspace(const tnrd_model* md, cudaStream_t s, const std::vect
 }
 
 
+
+#endif  // TNRD_EXPERIMENTS
 
 // Launch with programmatic stream serialization: the kernel may be scheduled
 // while its predecessor on the stream drains, and waits for it with
@@ -795,6 +819,7 @@ struct StageKernel {
         return TNRD_OK;
     }
 
+#ifdef TNRD_EXPERIMENTS
     // all T stages in one persistent dataflow launch (+ the setup kernel)
     static int launch_fused(const tnrd_model* md, const StageArgs* st, int nst, int batch,
                             cudaStream_t s) {
@@ -855,6 +880,8 @@ struct StageKernel {
         g_launches.fetch_add(2);
         return TNRD_OK;
     }
+
+#endif  // TNRD_EXPERIMENTS
 
     static long tiles(const StageArgs& a, int batch) {
         return (long)((a.W + TW - 1) / TW) * ((a.H + TH - 1) / TH) * batch;
@@ -1004,8 +1031,7 @@ static int split_workspace(const tnrd_model* md, cudaStream_t s, size_t bytes, v
         if (cs != cudaStreamCaptureStatusNone)
             return fail(TNRD_ECUDA, "split workspace must be allocated before stream capture");
         if (b.ptr) {
-            CUDA_TRY(cudaStreamSynchronize(s));
-            cudaFree(b.ptr);
+            md->retired.push_back(b.ptr);   // a captured graph may still use it
             b.ptr = nullptr;
             b.bytes = 0;
         }
@@ -1037,6 +1063,7 @@ static int dispatch_m(const tnrd_model* md, const StageArgs& a, int batch, cudaS
                   : dispatch_split_m_t<FAST, SmallTile>(m, a, batch, ws, s);
 }
 
+#ifdef TNRD_EXPERIMENTS
 template <int MS>
 struct StageKernelTC {
     using C = tc::TcCfg<MS>;
@@ -1261,8 +1288,7 @@ static int launch_zf(const tnrd_model* md, int t, const StageArgs& a, int batch,
             if (cs != cudaStreamCaptureStatusNone)
                 return fail(TNRD_ECUDA, "z-field workspace must be allocated before stream capture");
             if (b.ptr) {
-                CUDA_TRY(cudaStreamSynchronize(s));
-                cudaFree(b.ptr);
+                md->retired.push_back(b.ptr);   // a captured graph may still use it
                 b.ptr = nullptr;
                 b.bytes = 0;
             }
@@ -1339,6 +1365,14 @@ static int launch_zf(const tnrd_model* md, int t, const StageArgs& a, int batch,
 }
 
 
+#else
+extern "C" int tnrd_set_zfield_passes(int n) {
+    (void)n;
+    return fail(TNRD_EUNSUPPORTED, "z-field kernel not built (TNRD_EXPERIMENTS)");
+}
+
+#endif  // TNRD_EXPERIMENTS
+
 static int check_shape(const tnrd_model* md, int batch, int H, int W, int64_t ld,
                        int64_t image_stride) {
     if (batch < 1 || batch > 65535) return fail(TNRD_EINVAL, "batch must be in [1, 65535], got %d", batch);
@@ -1392,21 +1426,25 @@ static StageArgs stage_args(const tnrd_model* md, int t, uint32_t flags) {
     a.flags = flags;
     a.stage = t;
     a.status = nullptr;
+    a.force_out = nullptr;
     return a;
 }
 
 static int launch_stage(const tnrd_model* md, int t, const float* u_in, const float* f,
                         float* u_out, int batch, int H, int W, int64_t ld, int64_t image_stride,
-                        uint32_t flags, uint32_t* d_status, cudaStream_t s) {
+                        uint32_t flags, uint32_t* d_status, cudaStream_t s, float* force_out = nullptr) {
     StageArgs a = stage_args(md, t, flags);
     a.u_in = u_in; a.f = f; a.u_out = u_out;
+    a.force_out = force_out;
     a.ld = ld; a.img_stride = image_stride;
     a.H = H; a.W = W;
     a.status = d_status;
     const int mode = g_kernel_mode.load();
+#ifdef TNRD_EXPERIMENTS
     if (mode == 2 && tc3_supported(md)) return dispatch_tc3(md, t, a, batch, s);
     if (mode == 5 && tc_supported(md)) return dispatch_tc(md, t, a, batch, s);
     if (mode == 8 && zf_supported(md)) return launch_zf(md, t, a, batch, s);
+#endif
     if (mode == 2 || mode == 5 || mode == 8)
         return fail(TNRD_EUNSUPPORTED, "tensor-core stage kernel unavailable for this model");
     return md->fast ? dispatch_m<true>(md, a, batch, s) : dispatch_m<false>(md, a, batch, s);
@@ -1426,6 +1464,27 @@ extern "C" int tnrd_stage(const tnrd_model* md, int t, const float* u_in, const 
                         (cudaStream_t)stream);
 }
 
+// diffusion_step with its force (diffusion.py:184-194 returns u_next and,
+// through the trace, u~ = u - force): both outputs from one launch.
+extern "C" int tnrd_stage_force(const tnrd_model* md, int t, const float* u_in, const float* f,
+                                float* u_out, float* force_out, int batch, int H, int W, int64_t ld,
+                                int64_t image_stride, uint32_t flags, uint32_t* d_status, void* stream) {
+    if (!md) return fail(TNRD_EINVAL, "model is NULL");
+    if (t < 0 || t >= md->T) return fail(TNRD_EINVAL, "stage %d out of range [0, %d)", t, md->T);
+    if (!u_in || !f || !u_out || !force_out || !d_status) return fail(TNRD_EINVAL, "NULL buffer");
+    if (u_in == u_out || force_out == u_out || force_out == u_in)
+        return fail(TNRD_EINVAL, "u_in, u_out and force_out must not alias");
+    if (flags & TNRD_STAGE_FORCE) return fail(TNRD_EINVAL, "TNRD_STAGE_FORCE makes u_out the force already");
+    int rc = check_shape(md, batch, H, W, ld, image_stride);
+    if (rc) return rc;
+    if (g_kernel_mode.load() == 2 || g_kernel_mode.load() == 5 || g_kernel_mode.load() == 8)
+        return fail(TNRD_EUNSUPPORTED, "tnrd_stage_force runs the CUDA-core stage kernels only");
+    DeviceGuard dg(md->device);
+    return launch_stage(md, t, u_in, f, u_out, batch, H, W, ld, image_stride, flags, d_status,
+                        (cudaStream_t)stream, force_out);
+}
+
+#ifdef TNRD_EXPERIMENTS
 // One fused dataflow launch for all T stages (mode 9).  Returns -1 when not
 // applicable.
 template <bool FAST>
@@ -1465,6 +1524,15 @@ static int despeckle_fused(const tnrd_model* md, const float* f, float* u_out, f
     return md->fast ? despeckle_fused_m<true>(md, st, batch, s) : despeckle_fused_m<false>(md, st, batch, s);
 }
 
+#else
+static int despeckle_fused(const tnrd_model* md, const float*, float*, float*, int, int, int, int64_t,
+                           int64_t, uint32_t*, cudaStream_t) {
+    (void)md;
+    if (g_kernel_mode.load() == 9) return fail(TNRD_EUNSUPPORTED, "fused dataflow kernel not built (TNRD_EXPERIMENTS)");
+    return -1;
+}
+#endif  // TNRD_EXPERIMENTS
+
 static int despeckle_stages(const tnrd_model* md, const float* f, float* u_out, float* work,
                             int batch, int H, int W, int64_t ld, int64_t image_stride,
                             uint32_t* d_status, cudaStream_t s) {
@@ -1491,6 +1559,10 @@ static const tnrd_model::ForkRes* batch_fork(const tnrd_model* md, int batch, in
         return !(e && e[0] == '0');
     }();
     if (!enabled || batch < 2 || g_kernel_mode.load() != 0) return nullptr;
+    // the fork resources are keyed by the caller's stream handle: the
+    // per-thread default stream is a different stream in every thread under
+    // one handle, so it never forks
+    if (s == cudaStreamPerThread) return nullptr;
     StageArgs a = stage_args(md, 0, 0u);
     a.H = H; a.W = W;
     if (cc_variant(a, batch / 2) != 1) return nullptr;
@@ -1737,6 +1809,12 @@ static int plan_banded_host(tnrd_plan* p, const float* f_host, float* u_host, in
     const tnrd_model* md = p->md;
     int rc = banded_setup(p, nb);
     if (rc) return rc;
+    // work queued earlier on the plan's stream (tnrd_plan_despeckle_device
+    // returns without a sync) uses the same buffers: the copy and band
+    // streams start after it
+    CUDA_TRY(cudaEventRecord(p->ev_reset, p->stream));
+    CUDA_TRY(cudaStreamWaitEvent(p->copy_in, p->ev_reset, 0));
+    for (cudaStream_t bs : p->band_streams) CUDA_TRY(cudaStreamWaitEvent(bs, p->ev_reset, 0));
     const int H = p->H, W = p->W, T = md->T;
     const int row_tiles = (H + LargeTile::TH - 1) / LargeTile::TH;
     std::vector<int> r0(nb + 1);
@@ -2186,11 +2264,7 @@ __global__ void prox_kernel(const float* __restrict__ ut, const float* __restric
                             float* __restrict__ out, int64_t n, float lam4, float c8, float inv2a) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const float u = ut[i];
-        const float ff = fmaxf(f[i], kFFloor);
-        const float fl2 = ff * ff;
-        const float root = sqrtf(fmaf(u, u, c8 * fl2));
-        out[i] = u >= 0.0f ? (u + root) * inv2a : (lam4 * fl2) / (root - u);
+        out[i] = prox_idiv_f(ut[i], f[i], lam4, c8, inv2a);
     }
 }
 

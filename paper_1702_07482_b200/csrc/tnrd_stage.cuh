@@ -109,6 +109,7 @@ struct StageArgs {
     uint32_t flags;
     int stage;
     uint32_t* status;    // [0] first non-finite stage (atomicMin), [1] f flags (atomicAnd ~bit)
+    float* force_out;    // optional second output: the force (tnrd_stage_force), same layout as u_out
 };
 
 __device__ __forceinline__ float ex2f(float x) {
@@ -139,22 +140,53 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-// Reaction step of one pixel: the I-divergence prox (speckle.py:111-121,
-// cancellation-free for u~ < 0) or, with TNRD_STAGE_PROJECTED, the projected
-// comparison variant u' = smooth_max(u - force - lam (1/u - f^2/u^3), floor)
-// with smooth_max(x, c) = c + tau log(1 + exp((x - c)/tau)), tau = 0.01 c
-// (diffusion.py:149-168, 197-216).  `fv` is the raw observation.
+// I-divergence prox (speckle.py:111-121): u' = (u~ + sqrt(u~^2 + 8 a lam
+// f^2)) / (2a), f floored at 1e-6, evaluated cancellation-free for u~ < 0
+// as 4 lam f^2 / (root - u~).  The reference squares in float64, so it
+// stays finite wherever its result fits; fp32 squares overflow once |u~| or
+// f exceeds ~1e19.  When |u~| > 2^60 or 8 a lam f^2 overflows (rare: the
+// branch is uniform in practice) u~ and f are scaled by an exact power of
+// two 2^-E, E = exponent of max(|u~|, f), and the result is scaled back:
+// finite whenever the true result fits in fp32; non-finite for a non-finite
+// u~ (the reference's inf / nan) or a result beyond the fp32 range.
+__device__ __forceinline__ float prox_idiv_f(float ut, float fv, float lam4, float c8, float inv2a) {
+    const float ff = fmaxf(fv, kFFloor);
+    const float fl2 = ff * ff;
+    const float q = c8 * fl2;
+    if (fabsf(ut) <= 1.152921504606847e18f && q <= 3.4028234663852886e38f) {   // 2^60, FLT_MAX
+        const float root = sqrtf(fmaf(ut, ut, q));
+        return ut >= 0.0f ? (ut + root) * inv2a : (lam4 * fl2) / (root - ut);
+    }
+    if (!(fabsf(ut) < __int_as_float(0x7f800000))) return ut - ut;   // +-inf, nan -> nan
+    // s = 2^-E (exponent field 254 - e, at least 1), 1/s = 2^E exactly
+    const int eb = __float_as_int(fmaxf(fabsf(ut), ff)) & 0x7f800000;
+    const int sb = max(0x7f000000 - eb, 0x00800000);
+    const float s = __int_as_float(sb);
+    const float inv_s = __int_as_float(0x7f000000 - sb);
+    const float uts = ut * s, ffs = ff * s;
+    const float fs2 = ffs * ffs;
+    const float root = sqrtf(fmaf(uts, uts, c8 * fs2));
+    // u~ < 0: 4 lam f^2 / (root - u~) = 4 lam f * (f s / ((root - u~) s)):
+    // no square of the (possibly underflowing) scaled f
+    return ut >= 0.0f ? ((uts + root) * inv2a) * inv_s : (lam4 * ff) * (ffs / (root - uts));
+}
+
+// Reaction step of one pixel: the I-divergence prox above or, with
+// TNRD_STAGE_PROJECTED, the projected comparison variant
+// u' = smooth_max(u - force - lam (1/u - f^2/u^3), floor) with
+// smooth_max(x, c) = c + tau log(1 + exp((x - c)/tau)), tau = 0.01 c
+// (diffusion.py:149-168, 197-216); f^2/u^3 is formed as (f/u)^2 / u so it
+// does not overflow before the float64 reference would.  `fv` is the raw
+// observation.
 __device__ __forceinline__ float reaction(float u, float force, float fv, const StageArgs& p) {
     if (p.flags & 0x20u) {
-        const float ut = u - force - p.lam * (1.0f / u - (fv * fv) / (u * u * u));
+        const float iu = 1.0f / u;
+        const float fu = fv * iu;
+        const float ut = u - force - p.lam * (iu - fu * fu * iu);
         const float x = (ut - p.pfloor) * p.inv_tau;
         return fmaf(p.tau, fmaxf(x, 0.0f) + log1pf(expf(-fabsf(x))), p.pfloor);
     }
-    const float ff = fmaxf(fv, kFFloor);
-    const float ut = u - force;
-    const float fl2 = ff * ff;
-    const float root = sqrtf(fmaf(ut, ut, p.c8 * fl2));
-    return ut >= 0.0f ? (ut + root) * p.inv2a : (p.lam4 * fl2) / (root - ut);
+    return prox_idiv_f(u - force, fv, p.lam4, p.c8, p.inv2a);
 }
 
 // Half-sample symmetric reflection (np.pad mode="symmetric", one fold) and
@@ -597,7 +629,9 @@ __device__ __forceinline__ bool reduce_splits(float* red, int split, int obx, in
 // epilogue of one pixel: u~ = u - force, reaction, checks, store
 __device__ __forceinline__ void finish_pixel(const StageArgs& p, float u, float force,
                                              const float* __restrict__ fin, float* uout,
-                                             int64_t off, bool& bad, uint32_t& fbits) {
+                                             int64_t off, bool& bad, uint32_t& fbits,
+                                             float* fout = nullptr) {
+    if (fout) fout[off] = force;
     float res;
     if (p.flags & 0x8u) {
         res = force;
@@ -615,7 +649,9 @@ __device__ __forceinline__ void finish_pixel(const StageArgs& p, float u, float 
 
 // finish_pixel with the observation already loaded
 __device__ __forceinline__ void finish_pixel_f(const StageArgs& p, float u, float force, float fv,
-                                               float* uout, int64_t off, bool& bad, uint32_t& fbits) {
+                                               float* uout, int64_t off, bool& bad, uint32_t& fbits,
+                                               float* fout = nullptr) {
+    if (fout) fout[off] = force;
     float res;
     if (p.flags & 0x8u) {
         res = force;
@@ -703,6 +739,7 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
     const float* __restrict__ uin = p.u_in + (int64_t)img * p.img_stride;
     const float* __restrict__ fin = p.f + (int64_t)img * p.img_stride;
     float* __restrict__ uout = p.u_out + (int64_t)img * p.img_stride;
+    float* fout = p.force_out ? p.force_out + (int64_t)img * p.img_stride : nullptr;
     const bool top_halo = p.flags & 0x2u;
     const bool bot_halo = p.flags & 0x4u;
 
@@ -761,7 +798,7 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
             const int X = X0 + ox0 + c;
             if (X >= p.W) continue;
             finish_pixel(p, sU[(oy0 + r + 2 * R) * C::US + ox0 + c + 2 * R], force[r][c], fin, uout,
-                         (int64_t)Y * p.ld + X, bad, fbits);
+                         (int64_t)Y * p.ld + X, bad, fbits, fout);
         }
     }
     report(p, bad, fbits);
@@ -1011,6 +1048,7 @@ __global__ void __launch_bounds__(128) stage_reduce_kernel(const StageArgs p, co
         const float* __restrict__ uin = p.u_in + (int64_t)img * p.img_stride;
         const float* __restrict__ fin = p.f + (int64_t)img * p.img_stride;
         float* __restrict__ uout = p.u_out + (int64_t)img * p.img_stride;
+        float* fout = p.force_out ? p.force_out + (int64_t)img * p.img_stride : nullptr;
         float uq[4], fq[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -1043,7 +1081,7 @@ __global__ void __launch_bounds__(128) stage_reduce_kernel(const StageArgs p, co
             if (X >= p.W) continue;
             float u = uq[c];
             if (p.flags & 0x1u) u = fmaxf(u, p.u0_floor);
-            finish_pixel_f(p, u, fa[c], fq[c], uout, (int64_t)Y * p.ld + X, bad, fbits);
+            finish_pixel_f(p, u, fa[c], fq[c], uout, (int64_t)Y * p.ld + X, bad, fbits, fout);
         }
     }
     report(p, bad, fbits);

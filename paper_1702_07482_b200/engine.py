@@ -40,6 +40,15 @@ def _stream_handle(stream=None) -> ctypes.c_void_p:
     return ctypes.c_void_p(s.cuda_stream)
 
 
+def stream_ctx(stream=None):
+    """Make ``stream`` current for the duration of a call: temporaries are
+    then allocated on the stream their kernels run on (the caching
+    allocator reuses a freed block only in that stream's order) and a status
+    read (.cpu()) is ordered after those kernels."""
+    import contextlib
+    return contextlib.nullcontext() if stream is None else torch().cuda.stream(stream)
+
+
 def _ptr(tensor) -> ctypes.c_void_p:
     return ctypes.c_void_p(tensor.data_ptr())
 
@@ -161,7 +170,9 @@ class DeviceModel:
         return self.m // 2
 
     def status(self) -> Status:
-        key = threading.get_ident()
+        # one status block per (thread, current stream): calls on different
+        # streams never share one
+        key = (threading.get_ident(), torch().cuda.current_stream(self.device).cuda_stream)
         s = self._status.get(key)
         if s is None:
             s = self._status[key] = Status(self.device)
@@ -187,7 +198,12 @@ class DeviceModel:
     def despeckle(self, f, out=None, work=None, stream=None, check=True):
         """run_diffusion on device tensors: f (H, W) or (B, H, W) fp32 CUDA.
         Returns u_T (same shape).  With check=False the status block is left
-        for a later ``status().check()`` (no host synchronisation)."""
+        for a later ``status().check()`` on the same stream (no host
+        synchronisation).  ``stream``: run (and allocate temporaries) there."""
+        with stream_ctx(stream):
+            return self._despeckle(f, out, work, check)
+
+    def _despeckle(self, f, out, work, check):
         t = torch()
         self._check_tensor(f, "f")
         B, H, W = self._shape(f)
@@ -199,17 +215,21 @@ class DeviceModel:
             if x is not None:
                 self._check_tensor(x, name)
                 if x.shape != f.shape or x.stride() != out.stride():
-                    raise ValueError(f"{name} must match f's shape/strides")
+                    raise ValueError(f"{name} must match f's shape and out's strides")
         if f.stride() != out.stride():
-            f = f.contiguous()
-        ld = f.stride(-2)
-        img_stride = f.stride(0) if f.dim() == 3 else ld * H
+            # the kernels take ONE row / image stride for f, out and work
+            f2 = t.empty_strided(out.shape, out.stride(), dtype=f.dtype, device=f.device)
+            f2.copy_(f)
+            f = f2
+        assert f.stride() == out.stride() and (work is None or work.stride() == out.stride())
+        ld = out.stride(-2)
+        img_stride = out.stride(0) if out.dim() == 3 else ld * H
         st = self.status()
-        st.reset(stream)
+        st.reset()
         _lib.check(_lib.load().tnrd_despeckle(
             self.handle, _ptr(f), _ptr(out),
             _ptr(work) if work is not None else None, B, H, W, ld, img_stride,
-            _ptr(st.buf), _stream_handle(stream)))
+            _ptr(st.buf), _stream_handle()))
         if check:
             st.check()
         return out
@@ -219,6 +239,18 @@ class DeviceModel:
         """One stage on device tensors.  ``rows`` = (row0, H) restricts the
         stage to rows [row0, row0 + H) of u/f/out (row strips: u must then
         carry the halo rows around that window when TOP/BOTTOM_HALO is set)."""
+        with stream_ctx(stream):
+            return self._stage(t_index, u, f, out, flags, status, rows)
+
+    def stage_force(self, t_index: int, u, f, stream=None):
+        """One stage returning (u_next, force) from ONE launch
+        (tnrd_stage_force): diffusion_step's output and the force behind its
+        trace's u~ = u - force."""
+        with stream_ctx(stream):
+            force = torch().empty_like(u)
+            return self._stage(t_index, u, f, None, 0, None, None, force_out=force), force
+
+    def _stage(self, t_index, u, f, out, flags, status, rows, force_out=None):
         t = torch()
         self._check_tensor(u, "u")
         self._check_tensor(f, "f")
@@ -236,12 +268,22 @@ class DeviceModel:
         off = row0 * ld * u.element_size()
         st = status if status is not None else self.status()
         if status is None:
-            st.reset(stream)
-        _lib.check(_lib.load().tnrd_stage(
-            self.handle, int(t_index), ctypes.c_void_p(u.data_ptr() + off),
-            ctypes.c_void_p(f.data_ptr() + off),
-            ctypes.c_void_p(out.data_ptr() + off), B, H, W, ld, img_stride,
-            int(flags), _ptr(st.buf), _stream_handle(stream)))
+            st.reset()
+        if force_out is not None:
+            self._check_tensor(force_out, "force_out")
+            if force_out.stride() != out.stride():
+                raise ValueError("force_out must share out's strides")
+            _lib.check(_lib.load().tnrd_stage_force(
+                self.handle, int(t_index), ctypes.c_void_p(u.data_ptr() + off),
+                ctypes.c_void_p(f.data_ptr() + off), ctypes.c_void_p(out.data_ptr() + off),
+                ctypes.c_void_p(force_out.data_ptr() + off), B, H, W, ld, img_stride,
+                int(flags), _ptr(st.buf), _stream_handle()))
+        else:
+            _lib.check(_lib.load().tnrd_stage(
+                self.handle, int(t_index), ctypes.c_void_p(u.data_ptr() + off),
+                ctypes.c_void_p(f.data_ptr() + off),
+                ctypes.c_void_p(out.data_ptr() + off), B, H, W, ld, img_stride,
+                int(flags), _ptr(st.buf), _stream_handle()))
         if status is None:
             st.check()
         return out

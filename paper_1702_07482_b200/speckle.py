@@ -104,6 +104,12 @@ def sample_speckle_device(clean, cfg: SpeckleConfig, out=None, stream=None,
     index b*H*W + y*W + x, so a batch equals its images generated with the
     matching index offsets, for any launch geometry.  ``clean=None`` is not
     accepted here; see speckle_field_device."""
+    from .engine import stream_ctx
+    with stream_ctx(stream):
+        return _sample_speckle_device(clean, cfg, out, check)
+
+
+def _sample_speckle_device(clean, cfg, out, check):
     from .engine import Status
     t = torch()
     require_cuda()
@@ -121,11 +127,11 @@ def sample_speckle_device(clean, cfg: SpeckleConfig, out=None, stream=None,
     img_stride = clean.stride(0) if clean.dim() == 3 else ld * H
     st = Status(clean.device) if check else None
     if st is not None:
-        st.reset(stream)
+        st.reset()
     _lib.check(_lib.load().tnrd_sample_speckle(
         _ptr(clean), _ptr(out), B, H, W, ld, img_stride, int(cfg.looks),
         _seed_u64(cfg), _ptr(st.buf) if st is not None else None,
-        _stream_handle(stream)))
+        _stream_handle()))
     if st is not None:
         host = st.buf.cpu().numpy().view(np.uint32)
         if host[1] != 0xFFFFFFFF:
@@ -136,6 +142,12 @@ def sample_speckle_device(clean, cfg: SpeckleConfig, out=None, stream=None,
 def speckle_field_device(shape, cfg: SpeckleConfig, device=None, stream=None):
     """The amplitude speckle field n (fp32, shape (H, W) or (B, H, W)) on
     the GPU: sqrt(Gamma(L, 1/L)) per pixel."""
+    from .engine import stream_ctx
+    with stream_ctx(stream):
+        return _speckle_field_device(shape, cfg, device)
+
+
+def _speckle_field_device(shape, cfg, device):
     t = torch()
     require_cuda()
     shape = tuple(int(v) for v in shape)
@@ -145,7 +157,7 @@ def speckle_field_device(shape, cfg: SpeckleConfig, device=None, stream=None):
     B, H, W = (1, *shape) if len(shape) == 2 else shape
     _lib.check(_lib.load().tnrd_sample_speckle(
         None, _ptr(out), B, H, W, W, H * W, int(cfg.looks), _seed_u64(cfg),
-        None, _stream_handle(stream)))
+        None, _stream_handle()))
     return out
 
 

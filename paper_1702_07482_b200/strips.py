@@ -87,6 +87,33 @@ def exchange_halos(buf, layout: StripLayout, group=None) -> None:
             req.wait()
 
 
+def exchange_halos_host(buf, layout: StripLayout, group=None) -> None:
+    """exchange_halos through host memory: the boundary rows are copied to
+    CPU tensors, exchanged with a CPU backend (gloo) and copied back.  For
+    process groups without device P2P (gloo, or several ranks sharing one
+    GPU in bench.py's TNRD_BENCH_SHARED_GPU functional check)."""
+    import torch.distributed as dist
+    h, n = layout.halo, layout.n
+    ops, back = [], []
+    if layout.has_top:
+        up = layout.rank - 1
+        ops.append(dist.P2POp(dist.isend, buf[h:2 * h].cpu(), up, group))
+        rt = buf.new_empty((h,) + tuple(buf.shape[1:]), device="cpu")
+        ops.append(dist.P2POp(dist.irecv, rt, up, group))
+        back.append((slice(0, h), rt))
+    if layout.has_bottom:
+        down = layout.rank + 1
+        ops.append(dist.P2POp(dist.isend, buf[n:n + h].cpu(), down, group))
+        rb = buf.new_empty((h,) + tuple(buf.shape[1:]), device="cpu")
+        ops.append(dist.P2POp(dist.irecv, rb, down, group))
+        back.append((slice(n + h, n + 2 * h), rb))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for sl, t in back:
+        buf[sl].copy_(t)
+
+
 StageFn = Callable[[int, object, object, object, StripLayout, int], None]
 
 

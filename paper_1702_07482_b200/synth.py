@@ -161,3 +161,51 @@ def scene_crop(cfg: Config, y0: int, y1: int, x0: int, x1: int) -> np.ndarray:
             out[a - y0:b - y0, c - x0:d - x0] = fn[a - tr * T:b - tr * T,
                                                    c - tc * T:d - tc * T]
     return out
+
+
+# ---- parallel generation (host cores; numpy work per image / scene tile) ----
+
+def _pool(workers):
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+    import os
+    n = workers or min(32, os.cpu_count() or 1)
+    # fork: children only run numpy (call before any CUDA work in the parent
+    # where possible; they never touch the device)
+    return ProcessPoolExecutor(max_workers=n, mp_context=mp.get_context("fork")), n
+
+
+def _noisy_f(args):
+    cfg, i = args
+    return noisy_image(cfg, i)[1]
+
+
+def noisy_batch(cfg: Config, indices, workers: int | None = None) -> np.ndarray:
+    """fp32 observations of images ``indices`` of a batch config, stacked
+    (B, H, W); generated on all host cores (bit-identical to noisy_image)."""
+    indices = list(indices)
+    if len(indices) <= 2:
+        return np.stack([noisy_image(cfg, i)[1] for i in indices])
+    ex, _ = _pool(workers)
+    with ex:
+        return np.stack(list(ex.map(_noisy_f, [(cfg, i) for i in indices])))
+
+
+def _tile_f(args):
+    cfg, tr, tc = args
+    return tr, tc, scene_tile(cfg, tr, tc)[1]
+
+
+def scene_rows_parallel(cfg: Config, row0: int, row1: int, workers: int | None = None) -> np.ndarray:
+    """scene_rows(cfg, row0, row1) with the scene tiles generated on all
+    host cores (same values)."""
+    T = SCENE_TILE
+    nt = cfg.W // T
+    f = np.empty((row1 - row0, cfg.W), dtype=np.float32)
+    jobs = [(cfg, tr, tc) for tr in range(row0 // T, (row1 - 1) // T + 1) for tc in range(nt)]
+    ex, _ = _pool(workers)
+    with ex:
+        for tr, tc, fn in ex.map(_tile_f, jobs):
+            a, b = max(row0, tr * T), min(row1, (tr + 1) * T)
+            f[a - row0:b - row0, tc * T:(tc + 1) * T] = fn[a - tr * T:b - tr * T]
+    return f

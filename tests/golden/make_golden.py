@@ -198,6 +198,34 @@ def main(which):
             out[f"pc{m}"] = patch_correlation(img, adj, m)
         save("train_imageops", img=img, adj=adj, **out)
         print("wrote training fixtures")
+    if "overflow" in which:
+        # fp32 range edge of the error contract (diffusion.py:238-239,
+        # speckle.py:119-121): the reference squares u~ in float64
+        orng = np.random.default_rng(0)
+        f = orng.uniform(1, 255, (40, 40))
+        # weights 1e30: |u~| ~ 1e31 (u~^2 overflows fp32) but the reference
+        # finishes with a finite image (max ~1e29)
+        full_case("huge_weights", f, ref_model(3, 2, 3, 7, seed=1, weight_scale=1e30))
+        # stage 1 weights 1e300: the reference's u~^2 overflows float64 in
+        # stage 1 -> FloatingPointError("non-finite image after stage 1")
+        model = ref_model(3, 2, 3, 7, seed=1)
+        model.stages[1].weights *= 1e301
+        f32 = np.asarray(f, dtype=np.float32).astype(np.float64)
+        try:
+            sd.run_diffusion(f32, model)
+            msg = ""
+        except FloatingPointError as e:
+            msg = str(e)
+        assert msg, "expected the reference to raise"
+        save("overflow_stage1", f=f32, raises=msg, **pack_model(model))
+        # prox far outside the fp32 square range, results inside fp32
+        big = orng.uniform(-1, 1, (20, 20)) * 10.0 ** orng.uniform(15, 37, (20, 20))
+        fb = 10.0 ** orng.uniform(-3, 19, (20, 20))
+        big = np.asarray(big, dtype=np.float32).astype(np.float64)
+        fb = np.asarray(fb, dtype=np.float32).astype(np.float64)
+        save("prox_large", u_tilde=big, f=fb,
+             **{f"out_{i}": sd.prox_idiv(big, fb, lam) for i, lam in enumerate((0.3, 1.0, 10.0))},
+             lams=np.array([0.3, 1.0, 10.0]))
     for key in ("c1", "c2"):
         if key in which:
             cfg = synth.CONFIGS[key]

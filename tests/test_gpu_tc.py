@@ -9,7 +9,9 @@ from conftest import golden_model, golden_names, load_golden, parity_stats
 import paper_1702_07482_b200 as tn
 from paper_1702_07482_b200 import _lib, synth
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not _lib.has_experiments(),
+                                 reason="opt-in kernel not built (-DTNRD_EXPERIMENTS)")]
 
 REL_TOL = 1e-4
 PSNR_TOL = 0.01

@@ -129,6 +129,8 @@ def test_fused_dataflow_bit_identical_to_split_stages(cuda, shape):
     shared-memory taps and degree-7 RBF table: bit-identical output,
     including the projected variant."""
     torch = cuda
+    if not _lib.has_experiments():
+        pytest.skip("fused dataflow kernel not built (-DTNRD_EXPERIMENTS)")
     for variant in ("prox", "projected"):
         model = synth.make_model(7, 12, 4, 63, seed=len(shape) * 10 + shape[-1])
         model.variant = variant

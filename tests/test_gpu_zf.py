@@ -13,7 +13,9 @@ from paper_1702_07482_b200 import _lib, synth
 
 from test_gpu_strips import lockstep_strips
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not _lib.has_experiments(),
+                                 reason="opt-in kernel not built (-DTNRD_EXPERIMENTS)")]
 
 REL_TOL = 1e-4     # north_star: max relative error on output pixels
 PSNR_TOL = 0.01    # north_star: |dPSNR| in dB
