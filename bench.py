@@ -198,8 +198,16 @@ def cpu_worker(spec: str) -> None:
     t0 = time.perf_counter()
     O.run_diffusion(crop, model)
     dt = time.perf_counter() - t0
-    print(json.dumps({"seconds": dt, "t_end": time.time(),
-                      "peak_rss_mb": resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1024.0}))
+    # VmHWM (this process image's high-water mark): ru_maxrss would carry
+    # the forking parent's RSS across exec
+    hwm = None
+    with open("/proc/self/status") as fh:
+        for line in fh:
+            if line.startswith("VmHWM:"):
+                hwm = float(line.split()[1]) / 1024.0
+    if hwm is None:
+        hwm = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1024.0
+    print(json.dumps({"seconds": dt, "t_end": time.time(), "peak_rss_mb": hwm}))
 
 
 def _spawn_worker(workload, index, side, threads, start=0.0):

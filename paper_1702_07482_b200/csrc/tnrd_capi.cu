@@ -284,14 +284,17 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
     md->zlo = mu0 - 7.0 * gamma;
     const double zhi = mu0 + (M - 1) * delta + 7.0 * gamma;
     md->ni = (int)std::ceil((zhi - md->zlo) / md->h) + 1;
-    md->nip = round_up(md->ni, 8);   // whole 8-interval blocks (rbf_lo_offset)
+    // interval 0 and interval ni + 1 are all-zero guards: z beyond the fitted
+    // range (phi < 3e-11 sum|w| there) reads phi = 0 -- the reference's exp
+    // underflows to exactly 0 far out, which matters once |w| is huge
+    md->nip = round_up(md->ni + 2, 8);   // whole 8-interval blocks (rbf_lo_offset)
     md->fast = (size_t)md->nip * kPolyN * kF <= 16384;  // <= 64 KB per group buffer
     md->tab_stride = md->fast ? md->nip * kPolyN : round_up(M, 4);
 
     // cubic table (parameter-space-taps kernels): same range, h / 5
     md->h3 = std::min(delta, gamma) / kCubicSub;
     md->ni3 = (int)std::ceil((zhi - md->zlo) / md->h3) + 1;
-    md->tab3_stride = md->fast ? round_up(md->ni3, 8) * 4 : 0;
+    md->tab3_stride = md->fast ? round_up(md->ni3 + 2, 8) * 4 : 0;   // + the two zero guards
     if (md->tab3_stride > kMaxCubicStride) md->tab3_stride = 0;   // PT kernels off
 
     const size_t ntap = (size_t)T * md->nk_pad * md->kp;
@@ -314,7 +317,7 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
                     md->fit_err = std::max(md->fit_err,
                                            fit_interval(w, M, mu0, delta, gamma,
                                                         md->zlo + q * md->h, md->h,
-                                                        tb + rbf_lo_offset(q), &e32));
+                                                        tb + rbf_lo_offset(q + 1), &e32));
                     md->fit_err32 = std::max(md->fit_err32, e32);
                 }
             } else {
@@ -338,7 +341,7 @@ extern "C" int tnrd_model_create(int m, int nk, int T, int M, const double* kern
                         double e32 = 0.0;
                         e3[id] = std::max(e3[id], fit_interval<4, 9>(w, M, mu0, delta, gamma,
                                                                     md->zlo + q * md->h3, md->h3,
-                                                                    tb + 4 * q, &e32));
+                                                                    tb + 4 * (q + 1), &e32));
                         e3_32[id] = std::max(e3_32[id], e32);
                     }
                 }
@@ -1405,14 +1408,14 @@ static StageArgs stage_args(const tnrd_model* md, int t, uint32_t flags) {
     a.inv_h = (float)(1.0 / md->h);
     a.tab_bias = 0u - (0x4B400000u << 5);
     a.tab_ni = md->nip;
-    a.t_off = (float)(-md->zlo / md->h);
-    a.tmax = (float)(md->ni - 1);
+    a.t_off = (float)(1.0 - md->zlo / md->h);
+    a.tmax = (float)(md->ni + 1);
     a.tab3 = md->tab3_stride ? md->d_tab3 + (size_t)t * md->nk_pad * md->tab3_stride : nullptr;
     a.tab3_stride = md->tab3_stride;
     a.tab3_bias = 0u - (0x4B400000u << 4);
     a.inv_h3 = md->tab3_stride ? (float)(1.0 / md->h3) : 0.0f;
-    a.t_off3 = md->tab3_stride ? (float)(-md->zlo / md->h3) : 0.0f;
-    a.tmax3 = (float)(md->ni3 - 1);
+    a.t_off3 = md->tab3_stride ? (float)(1.0 - md->zlo / md->h3) : 0.0f;
+    a.tmax3 = (float)(md->ni3 + 1);
     a.delta = (float)md->delta;
     a.cE = (float)(-L2E / (2.0 * md->gamma * md->gamma));
     a.mu0 = (float)md->mu0;
