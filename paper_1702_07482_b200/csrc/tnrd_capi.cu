@@ -578,6 +578,12 @@ extern "C" int tnrd_status_decode(const uint32_t* h, int* bad_stage) {
 #ifndef TNRD_PT_SPLIT_F
 #define TNRD_PT_SPLIT_F 2
 #endif
+#ifndef TNRD_TILE_P2
+#define TNRD_TILE_P2 1
+#endif
+#ifndef TNRD_SPLIT_P2
+#define TNRD_SPLIT_P2 0
+#endif
 #ifndef TNRD_PT_TILE_MINB
 #define TNRD_PT_TILE_MINB 2
 #endif
@@ -765,7 +771,13 @@ struct StageKernel {
     // thread per output block, so the tap address is warp-uniform)
     // one thread per output block (no filter split: warp-uniform filter)
     static constexpr bool kPT = (T::TW / 4) * (T::TH / T::RB) == T::NT && FAST;
-    using TB = TapBlock<MS <= 7 ? 2560 : kMaxParamTaps>;
+    // FFMA2 row pairs with the pair-tap layout (tnrd_stage.cuh PairTaps,
+    // 3 <= m <= 7), per kernel as measured on B200: tile kernel on (C3
+    // +4.5%), split kernel off (C2 -3%)
+    static constexpr bool kP2Tile = PairTaps<MS>::kOn && TNRD_TILE_P2;
+    static constexpr bool kP2Split = PairTaps<MS>::kOn && TNRD_SPLIT_P2;
+    static constexpr int kTapFloats = PairTaps<MS>::kOn ? PairTaps<MS>::kFloats : C::KP;   // per filter (max)
+    using TB = TapBlock<MS <= 7 ? 4096 : kMaxParamTaps>;
     // forward blocking (measured on B200): m = 7 RF = 5 (252 blocks per
     // filter for 256 threads); m = 9 RF = 2 (C5 172.5 MPix/s; RF = 3 167.4,
     // RF = 6 144.4, RF = 4 138)
@@ -780,15 +792,30 @@ struct StageKernel {
     // htaps: this stage's taps on the host, [nk_pad][kp]
     static bool pt_fits(const StageArgs& a) {
         return kPT && param_taps_enabled() && a.tab3 != nullptr &&
-               (size_t)round_up(a.nk, 4) * C::KP <= sizeof(TB) / sizeof(float);
+               (size_t)round_up(a.nk, 4) * kTapFloats <= sizeof(TB) / sizeof(float);
     }
     // shared memory of the PT kernels: u | phi[f] | one cubic table for f filters
     template <class CC, int FF>
     static size_t pt_smem(const StageArgs& a) {
         return sizeof(float) * ((size_t)CC::SU + (size_t)FF * CC::SPHI + (size_t)FF * a.tab3_stride);
     }
-    static void fill_taps(TB& tb, const float* htaps, int nk) {
-        std::memcpy(tb.k, htaps, sizeof(float) * (size_t)round_up(nk, 4) * C::KP);
+    // htaps: [nk_pad][KP] row-major k; pairs: Q[A][B] = (k[A][B], k[A-1][B])
+    static void fill_taps(TB& tb, const float* htaps, int nk, bool pairs) {
+        const int n = round_up(nk, 4);
+        if (!pairs) {
+            std::memcpy(tb.k, htaps, sizeof(float) * (size_t)n * C::KP);
+        } else {
+            std::memset(tb.k, 0, sizeof(float) * (size_t)n * kTapFloats);
+            for (int i = 0; i < n; ++i) {
+                const float* k = htaps + (size_t)i * C::KP;
+                float* q = tb.k + (size_t)i * kTapFloats;
+                for (int A = 1; A < MS; ++A)
+                    for (int B = 0; B < MS; ++B) {
+                        q[2 * ((A - 1) * MS + B)] = k[A * MS + B];
+                        q[2 * ((A - 1) * MS + B) + 1] = k[(A - 1) * MS + B];
+                    }
+            }
+        }
     }
 
     static int launch(const StageArgs& a, int batch, cudaStream_t s, const float* htaps = nullptr) {
@@ -803,11 +830,11 @@ struct StageKernel {
             if (htaps && pt_fits(a)) {
                 static std::mutex mu2;
                 static uint64_t attr2 = 0;
-                auto kern = stage_kernel_pt<MS, TH, TW, RF_PT, RB, NT, FAST, F_TILE_PT, TNRD_PT_TILE_MINB, TB>;
+                auto kern = stage_kernel_pt<MS, TH, TW, RF_PT, RB, NT, FAST, F_TILE_PT, TNRD_PT_TILE_MINB, TB, kP2Tile>;
                 int rc = prepare(kern, dev, attr2, mu2);
                 if (rc) return rc;
                 TB tb;
-                fill_taps(tb, htaps, a.nk);
+                fill_taps(tb, htaps, a.nk, kP2Tile);
                 b.ngroups = (a.nk + F_TILE_PT - 1) / F_TILE_PT;
                 CUDA_TRY(launch_pdl(kern, grid, NT, pt_smem<CPT, F_TILE_PT>(a), s, b, tb));
                 g_launches.fetch_add(1);
@@ -903,9 +930,10 @@ struct StageKernel {
                 static std::mutex mu;
                 static uint64_t attr_set = 0;
                 static int occ[64] = {0};
-                auto kern = stage_kernel_split_pt<MS, TH, TW, RF_SPLIT_PT, RB, NT, FAST, F_SPLIT_PT, TNRD_PT_MINB, TB>;
+                auto kern = stage_kernel_split_pt<MS, TH, TW, RF_SPLIT_PT, RB, NT, FAST, F_SPLIT_PT, TNRD_PT_MINB, TB,
+                                                  kP2Split>;
                 TB tb;
-                fill_taps(tb, htaps, a.nk);
+                fill_taps(tb, htaps, a.nk, kP2Split);
                 return launch_split_k(kern, pt_smem<CPS, F_SPLIT_PT>(a), F_SPLIT_PT, a, batch, wsp, s, mu,
                                       attr_set, occ, tb);
             }

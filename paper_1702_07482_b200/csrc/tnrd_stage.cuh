@@ -468,15 +468,209 @@ __device__ __forceinline__ void forward_group(const StageArgs& p, const float* s
         forward_block<C, MS, RF, FAST, BATCH_ROWS>(p, sU, phif, k, tb, tabf, blk);
 }
 
+// ---- FFMA2 (fma.rn.f32x2, sm_100): two IEEE fma.rn lanes per instruction --
+// FFMA2 reaches the FFMA FLOP peak at half the issue slots (measured on
+// B200, tools/probes/ffma2_probe.cu: 71.6 vs 72.3 TFLOP/s), which leaves the
+// slots for the shared-memory loads and the RBF.  The parameter-space-taps
+// kernels (m <= 7) pair two OUTPUT ROWS of a block: lanes (row 2q, row
+// 2q + 1) share the input value (a broadcast register operand) and take two
+// taps from a uniform register pair.  Each lane is the same fma.rn on the
+// same operands in the same order as the scalar loop, so results are
+// bit-identical to the FFMA kernels.
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+    f2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float f2_lo(f2_t v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    (void)hi;
+    return lo;
+}
+__device__ __forceinline__ float f2_hi(f2_t v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    (void)lo;
+    return hi;
+}
+// d = a * b + c per lane
+__device__ __forceinline__ f2_t ffma2(f2_t a, f2_t b, f2_t c) {
+    f2_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+
+// Pair-tap layout of one filter (parameter space, m <= 7): for tap rows
+// A = 1..MS-1 and columns B, Q[A][B] = (k[A][B], k[A-1][B]) at float2 index
+// (A-1) MS + B; single taps are halves of pairs (k[0][B] = Q[1][B].y).
+template <int MS>
+struct PairTaps {
+    static constexpr bool kOn = MS >= 3 && MS <= 7;
+    static constexpr int kFloats = round_up(2 * (MS - 1) * MS, 4);   // per filter
+};
+template <int MS>
+__device__ __forceinline__ float2 qpair(const float* kq, int A, int B) {
+    return reinterpret_cast<const float2*>(kq)[(A - 1) * MS + B];
+}
+template <int MS>
+__device__ __forceinline__ float qsingle(const float* kq, int A, int B) {
+    return A >= 1 ? qpair<MS>(kq, A, B).x : qpair<MS>(kq, 1, B).y;
+}
+
+// forward_block with FFMA2 row pairs (pair taps, cubic RBF): rows (2q, 2q+1)
+// of the RF x 4 block; an odd last row runs scalar
+template <class C, int MS, int RF, int BATCH_ROWS>
+__device__ __forceinline__ void forward_block_p2(const StageArgs& p, const float* sU, float* phif,
+                                                 const float* kq, uint32_t tb, int blk) {
+    constexpr int R = C::R;
+    constexpr int NP = RF / 2;
+    constexpr bool ODD = (RF & 1) != 0;
+    static_assert(NP >= 1, "row pairs need RF >= 2");
+    const int by = blk / C::NBX;
+    const int bx = blk - by * C::NBX;
+    const int x0 = bx * 4, y0 = by * RF;
+    f2_t acc2[NP][4];
+    float accs[4];
+#pragma unroll
+    for (int q = 0; q < NP; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc2[q][c] = 0ull;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) accs[c] = 0.0f;
+#pragma unroll
+    for (int rr = 0; rr < RF + 2 * R; ++rr) {
+        float v[4 * C::NV];
+        const float* src = sU + (y0 + rr) * C::US + x0;
+#pragma unroll
+        for (int q = 0; q < C::NV; ++q) {
+            const float4 t = lds128(src + 4 * q);
+            v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+        }
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            const int a0 = rr - 2 * q;   // tap row of rot180(k) for output row 2q
+            if (a0 >= 1 && a0 <= MS - 1) {
+#pragma unroll
+                for (int b = 0; b < MS; ++b) {
+                    // (kf[a0][b], kf[a0-1][b]) = swap of Q[MS-a0][MS-1-b]
+                    const float2 t = qpair<MS>(kq, MS - a0, MS - 1 - b);
+                    const f2_t kk = f2_pack(t.y, t.x);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        acc2[q][c] = ffma2(f2_pack(v[c + b], v[c + b]), kk, acc2[q][c]);
+                }
+            } else if (a0 == 0 || a0 == MS) {
+                // one row of the pair: kf[0][b] (row 2q) or kf[MS-1][b] (row 2q+1)
+#pragma unroll
+                for (int b = 0; b < MS; ++b) {
+                    const float kk = qsingle<MS>(kq, a0 == 0 ? MS - 1 : 0, MS - 1 - b);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        float lo = f2_lo(acc2[q][c]), hi = f2_hi(acc2[q][c]);
+                        if (a0 == 0) lo = fmaf(kk, v[c + b], lo);
+                        else hi = fmaf(kk, v[c + b], hi);
+                        acc2[q][c] = f2_pack(lo, hi);
+                    }
+                }
+            }
+        }
+        if constexpr (ODD) {
+            const int a = rr - (RF - 1);
+            if (a >= 0 && a < MS) {
+#pragma unroll
+                for (int b = 0; b < MS; ++b) {
+                    const float kk = qsingle<MS>(kq, MS - 1 - a, MS - 1 - b);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) accs[c] = fmaf(kk, v[c + b], accs[c]);
+                }
+            }
+        }
+    }
+    float acc[RF][4];
+#pragma unroll
+    for (int q = 0; q < NP; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            acc[2 * q][c] = f2_lo(acc2[q][c]);
+            acc[2 * q + 1][c] = f2_hi(acc2[q][c]);
+        }
+    if constexpr (ODD) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[RF - 1][c] = accs[c];
+    }
+    float* dst = phif + y0 * C::PW + x0;
+    float4 o[RF];
+#pragma unroll
+    for (int r = 0; r < RF; ++r) {
+        o[r].x = rbf_cubic_s(acc[r][0], tb, p);
+        o[r].y = rbf_cubic_s(acc[r][1], tb, p);
+        o[r].z = rbf_cubic_s(acc[r][2], tb, p);
+        o[r].w = rbf_cubic_s(acc[r][3], tb, p);
+        if ((r + 1) % BATCH_ROWS == 0 || r == RF - 1) {
+#pragma unroll
+            for (int q = r - (r % BATCH_ROWS); q <= r; ++q)
+                *reinterpret_cast<float4*>(dst + q * C::PW) = o[q];
+        }
+    }
+}
+
+// backward_filter with FFMA2 row pairs: force2[q] = rows (2q, 2q+1)
+template <class C, int MS, int RB>
+__device__ __forceinline__ void backward_filter_p2(const float* ph, const float* kq, int ox0, int oy0,
+                                                   f2_t (&force2)[RB / 2][4]) {
+    constexpr int R = C::R;
+    static_assert(RB % 2 == 0, "row pairs");
+#pragma unroll
+    for (int rr = 0; rr < RB + 2 * R; ++rr) {
+        float v[4 * C::NV];
+        const float* src = ph + (oy0 + rr) * C::PW + ox0;
+#pragma unroll
+        for (int q = 0; q < C::NV; ++q) {
+            const float4 t = lds128(src + 4 * q);
+            v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+        }
+#pragma unroll
+        for (int q = 0; q < RB / 2; ++q) {
+            const int a0 = rr - 2 * q;   // tap row of k for output row 2q
+            if (a0 >= 1 && a0 <= MS - 1) {
+#pragma unroll
+                for (int b = 0; b < MS; ++b) {
+                    const float2 t = qpair<MS>(kq, a0, b);       // (k[a0][b], k[a0-1][b])
+                    const f2_t kk = f2_pack(t.x, t.y);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        force2[q][c] = ffma2(f2_pack(v[c + b], v[c + b]), kk, force2[q][c]);
+                }
+            } else if (a0 == 0 || a0 == MS) {
+#pragma unroll
+                for (int b = 0; b < MS; ++b) {
+                    const float kk = qsingle<MS>(kq, a0 == 0 ? 0 : MS - 1, b);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        float lo = f2_lo(force2[q][c]), hi = f2_hi(force2[q][c]);
+                        if (a0 == 0) lo = fmaf(kk, v[c + b], lo);
+                        else hi = fmaf(kk, v[c + b], hi);
+                        force2[q][c] = f2_pack(lo, hi);
+                    }
+                }
+            }
+        }
+    }
+}
+
 // forward with the taps in the parameter space: the group's filters one
 // after the other over all NT threads, so the filter (and with it the tap
 // address) is uniform across every warp
-template <class C, int MS, int RF, int F, int NT, bool FAST, int BATCH_ROWS = RF>
+template <class C, int MS, int RF, int F, int NT, bool FAST, bool P2, int BATCH_ROWS = RF>
 __device__ __forceinline__ void forward_group_pt(const StageArgs& p, const float* sU, float* sPhi,
                                                  const float* kg, const float* tabg, int tid) {
+    static_assert(!P2 || PairTaps<MS>::kOn, "pair taps need 3 <= m <= 7");
+    constexpr int KS = P2 ? PairTaps<MS>::kFloats : C::KP;   // tap floats per filter
 #pragma unroll 1
     for (int fi = 0; fi < F; ++fi) {
-        const float* k = kg + fi * C::KP;
+        const float* k = kg + fi * KS;
         const float* tabf = tabg + fi * p.tab3_stride;
         const uint32_t tb = static_cast<uint32_t>(__cvta_generic_to_shared(tabf)) + p.tab3_bias;
         float* phif = sPhi + fi * C::SPHI;
@@ -484,8 +678,12 @@ __device__ __forceinline__ void forward_group_pt(const StageArgs& p, const float
         // outside divergent branches): threads past the last block recompute
         // it and store the same values
 #pragma unroll 1
-        for (int b0 = 0; b0 < C::NBLK; b0 += NT)
-            forward_block<C, MS, RF, FAST, BATCH_ROWS, true>(p, sU, phif, k, tb, tabf, min(b0 + tid, C::NBLK - 1));
+        for (int b0 = 0; b0 < C::NBLK; b0 += NT) {
+            if constexpr (P2)
+                forward_block_p2<C, MS, RF, BATCH_ROWS>(p, sU, phif, k, tb, min(b0 + tid, C::NBLK - 1));
+            else
+                forward_block<C, MS, RF, FAST, BATCH_ROWS, true>(p, sU, phif, k, tb, tabf, min(b0 + tid, C::NBLK - 1));
+        }
     }
 }
 
@@ -581,21 +779,47 @@ __device__ __forceinline__ void backward_group(const float* sPhi, const float* t
     }
 }
 
+// force accumulators of the parameter-space kernels: FFMA2 row pairs
+// (m <= 7) or scalars
+template <int MS, int RB, bool P2>
+struct ForceAcc {
+    f2_t f2[RB / 2 > 0 ? RB / 2 : 1][4];
+    float f1[RB][4];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if constexpr (P2) {
+                    if (r % 2 == 0) f2[r / 2][c] = 0ull;
+                } else {
+                    f1[r][c] = 0.0f;
+                }
+            }
+    }
+    __device__ __forceinline__ float get(int r, int c) const {
+        if constexpr (P2) return (r & 1) ? f2_hi(f2[r >> 1][c]) : f2_lo(f2[r >> 1][c]);
+        else return f1[r][c];
+    }
+};
+
 // backward with parameter-space taps (no filter split: every thread walks
-// all of the group's filters, so the tap address is CTA-uniform)
-template <class C, int MS, int RB, int F>
+// all of the group's filters, so the tap address is CTA-uniform).  Not
+// unrolled (the kernel's hot loop stays within the instruction cache);
+// written with pointer increments and a __syncwarp, the form in which ptxas
+// keeps the taps in uniform registers (a plain indexed unroll-1 loop loads
+// them into per-thread registers with LDC)
+template <class C, int MS, int RB, int F, bool P2>
 __device__ __forceinline__ void backward_group_pt(const float* sPhi, const float* kg, int ox0, int oy0,
-                                                  float (&force)[RB][4]) {
+                                                  ForceAcc<MS, RB, P2>& acc) {
     static_assert(C::NSPLIT == 1, "parameter-space taps need one thread per output block");
-    // not unrolled (the kernel's hot loop stays within the instruction
-    // cache); written with pointer increments and a __syncwarp, the form in
-    // which ptxas keeps the taps in uniform registers (a plain indexed
-    // unroll-1 loop loads them into per-thread registers with LDC)
+    constexpr int KS = P2 ? PairTaps<MS>::kFloats : C::KP;
     const float* k = kg;
     const float* ph = sPhi;
 #pragma unroll 1
-    for (int fi = 0; fi < F; ++fi, k += C::KP, ph += C::SPHI) {
-        backward_filter<C, MS, RB>(ph, k, ox0, oy0, force);
+    for (int fi = 0; fi < F; ++fi, k += KS, ph += C::SPHI) {
+        if constexpr (P2) backward_filter_p2<C, MS, RB>(ph, k, ox0, oy0, acc.f2);
+        else backward_filter<C, MS, RB>(ph, k, ox0, oy0, acc.f1);
         __syncwarp();
     }
 }
@@ -720,7 +944,7 @@ __device__ __forceinline__ void tbar_wait(uint64_t* bar, uint32_t parity) {
 // ---- tile kernel: one CTA = one output tile, all filter groups -------------
 // PT: taps read from the parameter space (`kp` = this stage's TapBlock)
 // instead of being staged in shared memory and held in registers
-template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, bool PT>
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, bool PT, bool P2 = false>
 __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float* kp) {
     using C = StageCfg<MS, TH, TW, RF, RB, NT, F>;
     constexpr int R = C::R;
@@ -760,11 +984,14 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
     const int split = PT ? 0 : tid / (C::OBX * C::OBY);  // which filters of a group
     const int obx = tid % C::OBX, oby = (tid / C::OBX) % C::OBY;
     const int ox0 = obx * 4, oy0 = oby * RB;
+    constexpr int KS = P2 ? PairTaps<MS>::kFloats : C::KP;   // PT tap floats per filter
     float force[RB][4];
+    ForceAcc<MS, RB, P2> facc;   // PT: FFMA2 row pairs (P2) or scalars
 #pragma unroll
     for (int r = 0; r < RB; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) force[r][c] = 0.0f;
+    if constexpr (PT) facc.zero();
 
     for (int g = 0; g < p.ngroups; ++g) {
         const int buf = PT ? 0 : g & 1;
@@ -773,17 +1000,23 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
         __syncthreads();  // params of group g landed; previous bwd done with sPhi
         if constexpr (!PT)
             if (g + 1 < p.ngroups) prefetch_group<C, F, NT>(p, sTap, sTab, g + 1, buf ^ 1, tid);
-        const float* tapg = PT ? kp + g * F * C::KP : sTap + buf * F * C::KP;
+        const float* tapg = PT ? kp + g * F * KS : sTap + buf * F * C::KP;
         const float* tabg = sTab + buf * tabsz;
-        if constexpr (PT) forward_group_pt<C, MS, RF, F, NT, FAST>(p, sU, sPhi, tapg, tabg, tid);
+        if constexpr (PT) forward_group_pt<C, MS, RF, F, NT, FAST, P2>(p, sU, sPhi, tapg, tabg, tid);
         else forward_group<C, MS, RF, F, FAST>(p, sU, sPhi, tapg, tabg, tid);
         __syncthreads();
         // PT: the table is free -- fetch the next group's under fix-up + backward
         if constexpr (PT)
             if (tid == 0 && g + 1 < p.ngroups) tbar_fetch(sTab, p.tab3 + (size_t)(g + 1) * tabsz, tabsz, &tbar);
         fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
-        if constexpr (PT) backward_group_pt<C, MS, RB, F>(sPhi, tapg, ox0, oy0, force);
+        if constexpr (PT) backward_group_pt<C, MS, RB, F, P2>(sPhi, tapg, ox0, oy0, facc);
         else backward_group<C, MS, RB, F>(sPhi, tapg, split, ox0, oy0, force);
+    }
+    if constexpr (PT) {
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) force[r][c] = facc.get(r, c);
     }
     if (!reduce_splits<C, RB>(sPhi, split, obx, oby, force)) return;
 
@@ -819,9 +1052,9 @@ struct TapBlock {
     float k[N];
 };
 
-template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB, class TB>
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB, class TB, bool P2>
 __global__ void __launch_bounds__(NT, MINB) stage_kernel_pt(const StageArgs p, const __grid_constant__ TB tk) {
-    stage_tile_body<MS, TH, TW, RF, RB, NT, FAST, F, true>(p, tk.k);
+    stage_tile_body<MS, TH, TW, RF, RB, NT, FAST, F, true, P2>(p, tk.k);
 }
 
 // ---- split kernels: work units = (tile, filter group) ----------------------
@@ -940,7 +1173,7 @@ __device__ __forceinline__ void stage_split_body(const StageArgs& p, const Split
 // order, walked as tile segments (u staged in the outer loop) so that the
 // inner group loop holds only shared-memory traffic and the partial store:
 // ptxas then keeps the group index -- and the tap addresses -- uniform.
-template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F>
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, bool P2>
 __device__ __forceinline__ void stage_split_body_pt(const StageArgs& p, const SplitWs& ws, const float* kp) {
     using C = StageCfg<MS, TH, TW, RF, RB, NT, F>;
     constexpr int TPX = TH * TW;
@@ -984,26 +1217,23 @@ __device__ __forceinline__ void stage_split_body_pt(const StageArgs& p, const Sp
         for (int g = g0; g < gend; ++g, ++k) {
             tbar_wait(&tbar, k & 1);
             __syncthreads();  // table + u tile in smem; previous unit done with sPhi
-            const float* tapg = kp + g * F * C::KP;
+            const float* tapg = kp + g * F * (P2 ? PairTaps<MS>::kFloats : C::KP);
             const float* tabg = sTab;
             // all RF rows' table lookups before the phi stores (with the taps
             // out of the registers this pays here too: +1% C2 on B200)
-            forward_group_pt<C, MS, RF, F, NT, FAST>(p, sU, sPhi, tapg, tabg, tid);
+            forward_group_pt<C, MS, RF, F, NT, FAST, P2>(p, sU, sPhi, tapg, tabg, tid);
             __syncthreads();
             // the table is free: fetch the next unit's under fix-up + backward
             if (tid == 0 && k + 1 < nunits)
                 tbar_fetch(sTab, p.tab3 + (size_t)(g + 1 < ng ? g + 1 : 0) * tabsz, tabsz, &tbar);
             fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
-            float force[RB][4];
-#pragma unroll
-            for (int r = 0; r < RB; ++r)
-#pragma unroll
-                for (int cc = 0; cc < 4; ++cc) force[r][cc] = 0.0f;
-            backward_group_pt<C, MS, RB, F>(sPhi, tapg, ox0, oy0, force);
+            ForceAcc<MS, RB, P2> facc;
+            facc.zero();
+            backward_group_pt<C, MS, RB, F, P2>(sPhi, tapg, ox0, oy0, facc);
 #pragma unroll
             for (int r = 0; r < RB; ++r)
                 __stcg(reinterpret_cast<float4*>(dst + (size_t)g * TPX + r * TW),
-                       make_float4(force[r][0], force[r][1], force[r][2], force[r][3]));
+                       make_float4(facc.get(r, 0), facc.get(r, 1), facc.get(r, 2), facc.get(r, 3)));
         }
     }
 }
@@ -1013,10 +1243,10 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel_split(const StageArgs p
     stage_split_body<MS, TH, TW, RF, RB, NT, FAST, F>(p, ws);
 }
 
-template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB, class TB>
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB, class TB, bool P2>
 __global__ void __launch_bounds__(NT, MINB) stage_kernel_split_pt(const StageArgs p, const SplitWs ws,
                                                                  const __grid_constant__ TB tk) {
-    stage_split_body_pt<MS, TH, TW, RF, RB, NT, FAST, F>(p, ws, tk.k);
+    stage_split_body_pt<MS, TH, TW, RF, RB, NT, FAST, F, P2>(p, ws, tk.k);
 }
 
 // sum of a pixel quad's partials in group order, then the epilogue (u from
