@@ -578,11 +578,17 @@ extern "C" int tnrd_status_decode(const uint32_t* h, int* bad_stage) {
 #ifndef TNRD_PT_SPLIT_F
 #define TNRD_PT_SPLIT_F 2
 #endif
-#ifndef TNRD_TILE_P2
-#define TNRD_TILE_P2 1
+#ifndef TNRD_TILE_TM
+#define TNRD_TILE_TM 2
 #endif
-#ifndef TNRD_SPLIT_P2
-#define TNRD_SPLIT_P2 0
+#ifndef TNRD_SPLIT_TM
+#define TNRD_SPLIT_TM 0
+#endif
+#ifndef TNRD_TILE_TM_M9
+#define TNRD_TILE_TM_M9 3
+#endif
+#ifndef TNRD_SPLIT_TM_M9
+#define TNRD_SPLIT_TM_M9 0
 #endif
 #ifndef TNRD_PT_TILE_MINB
 #define TNRD_PT_TILE_MINB 2
@@ -771,13 +777,16 @@ struct StageKernel {
     // thread per output block, so the tap address is warp-uniform)
     // one thread per output block (no filter split: warp-uniform filter)
     static constexpr bool kPT = (T::TW / 4) * (T::TH / T::RB) == T::NT && FAST;
-    // FFMA2 row pairs with the pair-tap layout (tnrd_stage.cuh PairTaps,
-    // 3 <= m <= 7), per kernel as measured on B200: tile kernel on (C3
-    // +4.5%), split kernel off (C2 -3%)
-    static constexpr bool kP2Tile = PairTaps<MS>::kOn && TNRD_TILE_P2;
-    static constexpr bool kP2Split = PairTaps<MS>::kOn && TNRD_SPLIT_P2;
-    static constexpr int kTapFloats = PairTaps<MS>::kOn ? PairTaps<MS>::kFloats : C::KP;   // per filter (max)
-    using TB = TapBlock<MS <= 7 ? 4096 : kMaxParamTaps>;
+    // tap layout / FFMA2 mode per kernel (tnrd_stage.cuh TapLayout), as
+    // measured on B200 (profiles/r02_ffma2): tile kernel TNRD_TILE_TM
+    // (default 2: filter-pair forward + row-pair backward; C3 +7.7% over the
+    // scalar kernel, 1 = row pairs only +4.4%), m = 9 TNRD_TILE_TM_M9 (default
+    // 3: filter-pair forward, scalar backward on the same taps: C5 +7.9%);
+    // split kernel TNRD_SPLIT_TM (default 0: scalar; 1 / 2 / 3 measured
+    // C2 -2.5% / +-0 / -1.5%).  All modes give the scalar kernel's bits.
+    static constexpr int kTmTile = PairTaps<MS>::kOn ? TNRD_TILE_TM : TNRD_TILE_TM_M9;
+    static constexpr int kTmSplit = PairTaps<MS>::kOn ? TNRD_SPLIT_TM : TNRD_SPLIT_TM_M9;
+    using TB = TapBlock<kMaxParamTaps>;
     // forward blocking (measured on B200): m = 7 RF = 5 (252 blocks per
     // filter for 256 threads); m = 9 RF = 2 (C5 172.5 MPix/s; RF = 3 167.4,
     // RF = 6 144.4, RF = 4 138)
@@ -792,28 +801,44 @@ struct StageKernel {
     // htaps: this stage's taps on the host, [nk_pad][kp]
     static bool pt_fits(const StageArgs& a) {
         return kPT && param_taps_enabled() && a.tab3 != nullptr &&
-               (size_t)round_up(a.nk, 4) * kTapFloats <= sizeof(TB) / sizeof(float);
+               tap_floats<kTmTile, F_TILE_PT>(a.nk) <= sizeof(TB) / sizeof(float) &&
+               tap_floats<kTmSplit, F_SPLIT_PT>(a.nk) <= sizeof(TB) / sizeof(float);
     }
     // shared memory of the PT kernels: u | phi[f] | one cubic table for f filters
     template <class CC, int FF>
     static size_t pt_smem(const StageArgs& a) {
         return sizeof(float) * ((size_t)CC::SU + (size_t)FF * CC::SPHI + (size_t)FF * a.tab3_stride);
     }
-    // htaps: [nk_pad][KP] row-major k; pairs: Q[A][B] = (k[A][B], k[A-1][B])
-    static void fill_taps(TB& tb, const float* htaps, int nk, bool pairs) {
-        const int n = round_up(nk, 4);
-        if (!pairs) {
-            std::memcpy(tb.k, htaps, sizeof(float) * (size_t)n * C::KP);
-        } else {
-            std::memset(tb.k, 0, sizeof(float) * (size_t)n * kTapFloats);
-            for (int i = 0; i < n; ++i) {
-                const float* k = htaps + (size_t)i * C::KP;
-                float* q = tb.k + (size_t)i * kTapFloats;
-                for (int A = 1; A < MS; ++A)
-                    for (int B = 0; B < MS; ++B) {
-                        q[2 * ((A - 1) * MS + B)] = k[A * MS + B];
-                        q[2 * ((A - 1) * MS + B) + 1] = k[(A - 1) * MS + B];
-                    }
+    // floats of the TapBlock for nk filters in groups of FF (zero filters pad
+    // the last group)
+    template <int TM, int FF>
+    static size_t tap_floats(int nk) {
+        return (size_t)((nk + FF - 1) / FF) * TapLayout<MS, C::KP, FF, TM>::group;
+    }
+    // htaps: [nk_pad][KP] row-major k (zero rows past nk) -> layout TM
+    template <int TM, int FF>
+    static void fill_taps(TB& tb, const float* htaps, int nk) {
+        using TL = TapLayout<MS, C::KP, FF, TM>;
+        const int ng = (nk + FF - 1) / FF;
+        std::memset(tb.k, 0, sizeof(float) * tap_floats<TM, FF>(nk));
+        for (int g = 0; g < ng; ++g) {
+            float* grp = tb.k + (size_t)g * TL::group;
+            for (int fi = 0; fi < FF; ++fi) {
+                const float* k = htaps + (size_t)(g * FF + fi) * C::KP;   // nk_pad rows: in range
+                float* bw = grp + TL::bwd0 + fi * TL::per_filter;
+                if constexpr (TM == 0) {
+                    std::memcpy(bw, k, sizeof(float) * C::KP);
+                } else if constexpr (TM != 3) {
+                    for (int A = 1; A < MS; ++A)   // row pairs Q[A][B] = (k[A][B], k[A-1][B])
+                        for (int B = 0; B < MS; ++B) {
+                            bw[2 * ((A - 1) * MS + B)] = k[A * MS + B];
+                            bw[2 * ((A - 1) * MS + B) + 1] = k[(A - 1) * MS + B];
+                        }
+                }
+                if constexpr (TM >= 2)   // filter pairs FP[a][b] = (kf_0[a][b], kf_1[a][b])
+                    for (int a2 = 0; a2 < MS; ++a2)
+                        for (int b2 = 0; b2 < MS; ++b2)
+                            grp[2 * (a2 * MS + b2) + fi] = k[(MS - 1 - a2) * MS + (MS - 1 - b2)];
             }
         }
     }
@@ -830,11 +855,11 @@ struct StageKernel {
             if (htaps && pt_fits(a)) {
                 static std::mutex mu2;
                 static uint64_t attr2 = 0;
-                auto kern = stage_kernel_pt<MS, TH, TW, RF_PT, RB, NT, FAST, F_TILE_PT, TNRD_PT_TILE_MINB, TB, kP2Tile>;
+                auto kern = stage_kernel_pt<MS, TH, TW, RF_PT, RB, NT, FAST, F_TILE_PT, TNRD_PT_TILE_MINB, TB, kTmTile>;
                 int rc = prepare(kern, dev, attr2, mu2);
                 if (rc) return rc;
                 TB tb;
-                fill_taps(tb, htaps, a.nk, kP2Tile);
+                fill_taps<kTmTile, F_TILE_PT>(tb, htaps, a.nk);
                 b.ngroups = (a.nk + F_TILE_PT - 1) / F_TILE_PT;
                 CUDA_TRY(launch_pdl(kern, grid, NT, pt_smem<CPT, F_TILE_PT>(a), s, b, tb));
                 g_launches.fetch_add(1);
@@ -931,9 +956,9 @@ struct StageKernel {
                 static uint64_t attr_set = 0;
                 static int occ[64] = {0};
                 auto kern = stage_kernel_split_pt<MS, TH, TW, RF_SPLIT_PT, RB, NT, FAST, F_SPLIT_PT, TNRD_PT_MINB, TB,
-                                                  kP2Split>;
+                                                  kTmSplit>;
                 TB tb;
-                fill_taps(tb, htaps, a.nk, kP2Split);
+                fill_taps<kTmSplit, F_SPLIT_PT>(tb, htaps, a.nk);
                 return launch_split_k(kern, pt_smem<CPS, F_SPLIT_PT>(a), F_SPLIT_PT, a, batch, wsp, s, mu,
                                       attr_set, occ, tb);
             }

@@ -519,6 +519,97 @@ __device__ __forceinline__ float qsingle(const float* kq, int A, int B) {
     return A >= 1 ? qpair<MS>(kq, A, B).x : qpair<MS>(kq, 1, B).y;
 }
 
+// Tap layouts of the parameter-space kernels (TM = tap mode):
+//   0: row-major k per filter (KP floats), scalar FFMA
+//   1: row pairs per filter (PairTaps), FFMA2 over output-row pairs
+//   2: per group of F = 2 filters, the forward's FILTER pairs
+//      FP[a][b] = (kf_f0[a][b], kf_f1[a][b]) (kf = rot180 k, 2 MS^2 floats
+//      rounded to 4), then each filter's row pairs for the backward.  The
+//      forward computes both filters of the group per thread (one u-row load
+//      feeds both), FFMA2 over the filter pair; the backward runs row pairs.
+//   3: the filter pairs FP only (fits the parameter space for m = 9, Nk = 80);
+//      the backward runs scalar FFMA on the halves of FP (k = rot180 kf).
+template <int MS, int KP, int F, int TM>
+struct TapLayout {
+    static constexpr int KQ = PairTaps<MS>::kFloats;
+    static constexpr int FPF = round_up(2 * MS * MS, 4);
+    static constexpr int per_filter = TM == 0 ? KP : (TM == 3 ? 1 : KQ);   // backward taps per filter
+    static constexpr int bwd0 = TM == 2 ? FPF : 0;                         // backward taps offset in a group
+    static constexpr int group = TM == 2 ? FPF + F * KQ : (TM == 3 ? FPF : F * per_filter);
+    static_assert(TM < 2 || F == 2, "filter-pair forward needs 2 filters per group");
+    static_assert(TM == 0 || TM == 3 || PairTaps<MS>::kOn, "row pairs need 3 <= m <= 7");
+};
+
+// tap k_fi[i] (i = a MS + b) of a filter-pair block FP (TM 3): the rot180
+// partner kf[MS^2 - 1 - i], lane fi; `fp` is already offset by fi
+template <int MS>
+struct FpTap {
+    const float* fp;
+    __device__ __forceinline__ float operator[](int i) const { return fp[2 * (MS * MS - 1 - i)]; }
+};
+
+// forward of both filters of a group (TM 2): one RF x 4 block, z of filter
+// 0 / 1 in the low / high lane of each FFMA2 (same fma.rn chain per filter as
+// the scalar forward_block, so the same bits)
+template <class C, int MS, int RF, int BATCH_ROWS>
+__device__ __forceinline__ void forward_block_fp(const StageArgs& p, const float* sU, float* phi0, float* phi1,
+                                                 const float* kfp, uint32_t tb0, uint32_t tb1, int blk) {
+    constexpr int R = C::R;
+    const int by = blk / C::NBX;
+    const int bx = blk - by * C::NBX;
+    const int x0 = bx * 4, y0 = by * RF;
+    f2_t acc2[RF][4];
+#pragma unroll
+    for (int r = 0; r < RF; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc2[r][c] = 0ull;
+#pragma unroll
+    for (int rr = 0; rr < RF + 2 * R; ++rr) {
+        float v[4 * C::NV];
+        const float* src = sU + (y0 + rr) * C::US + x0;
+#pragma unroll
+        for (int q = 0; q < C::NV; ++q) {
+            const float4 t = lds128(src + 4 * q);
+            v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+        }
+#pragma unroll
+        for (int a = 0; a < MS; ++a) {
+            const int ro = rr - a;
+            if (ro >= 0 && ro < RF) {
+#pragma unroll
+                for (int b = 0; b < MS; ++b) {
+                    const float2 t = reinterpret_cast<const float2*>(kfp)[a * MS + b];
+                    const f2_t kk = f2_pack(t.x, t.y);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        acc2[ro][c] = ffma2(f2_pack(v[c + b], v[c + b]), kk, acc2[ro][c]);
+                }
+            }
+        }
+    }
+    float* d0 = phi0 + y0 * C::PW + x0;
+    float* d1 = phi1 + y0 * C::PW + x0;
+    float4 o0[RF], o1[RF];
+#pragma unroll
+    for (int r = 0; r < RF; ++r) {
+        o0[r].x = rbf_cubic_s(f2_lo(acc2[r][0]), tb0, p);
+        o0[r].y = rbf_cubic_s(f2_lo(acc2[r][1]), tb0, p);
+        o0[r].z = rbf_cubic_s(f2_lo(acc2[r][2]), tb0, p);
+        o0[r].w = rbf_cubic_s(f2_lo(acc2[r][3]), tb0, p);
+        o1[r].x = rbf_cubic_s(f2_hi(acc2[r][0]), tb1, p);
+        o1[r].y = rbf_cubic_s(f2_hi(acc2[r][1]), tb1, p);
+        o1[r].z = rbf_cubic_s(f2_hi(acc2[r][2]), tb1, p);
+        o1[r].w = rbf_cubic_s(f2_hi(acc2[r][3]), tb1, p);
+        if ((r + 1) % BATCH_ROWS == 0 || r == RF - 1) {
+#pragma unroll
+            for (int q = r - (r % BATCH_ROWS); q <= r; ++q) {
+                *reinterpret_cast<float4*>(d0 + q * C::PW) = o0[q];
+                *reinterpret_cast<float4*>(d1 + q * C::PW) = o1[q];
+            }
+        }
+    }
+}
+
 // forward_block with FFMA2 row pairs (pair taps, cubic RBF): rows (2q, 2q+1)
 // of the RF x 4 block; an odd last row runs scalar
 template <class C, int MS, int RF, int BATCH_ROWS>
@@ -663,26 +754,39 @@ __device__ __forceinline__ void backward_filter_p2(const float* ph, const float*
 // forward with the taps in the parameter space: the group's filters one
 // after the other over all NT threads, so the filter (and with it the tap
 // address) is uniform across every warp
-template <class C, int MS, int RF, int F, int NT, bool FAST, bool P2, int BATCH_ROWS = RF>
+template <class C, int MS, int RF, int F, int NT, bool FAST, int TM, int BATCH_ROWS = RF>
 __device__ __forceinline__ void forward_group_pt(const StageArgs& p, const float* sU, float* sPhi,
                                                  const float* kg, const float* tabg, int tid) {
-    static_assert(!P2 || PairTaps<MS>::kOn, "pair taps need 3 <= m <= 7");
-    constexpr int KS = P2 ? PairTaps<MS>::kFloats : C::KP;   // tap floats per filter
+    using TL = TapLayout<MS, C::KP, F, TM>;
+    if constexpr (TM >= 2) {
+        // both filters per thread: warp-uniform control flow (the uniform
+        // datapath is only used outside divergent branches): threads past
+        // the last block recompute it and store the same values
+        const uint32_t tb0 = static_cast<uint32_t>(__cvta_generic_to_shared(tabg)) + p.tab3_bias;
+        const uint32_t tb1 = static_cast<uint32_t>(__cvta_generic_to_shared(tabg + p.tab3_stride)) + p.tab3_bias;
 #pragma unroll 1
-    for (int fi = 0; fi < F; ++fi) {
-        const float* k = kg + fi * KS;
-        const float* tabf = tabg + fi * p.tab3_stride;
-        const uint32_t tb = static_cast<uint32_t>(__cvta_generic_to_shared(tabf)) + p.tab3_bias;
-        float* phif = sPhi + fi * C::SPHI;
-        // warp-uniform control flow (the uniform datapath is only used
-        // outside divergent branches): threads past the last block recompute
-        // it and store the same values
+        for (int b0 = 0; b0 < C::NBLK; b0 += NT)
+            forward_block_fp<C, MS, RF, BATCH_ROWS>(p, sU, sPhi, sPhi + C::SPHI, kg, tb0, tb1,
+                                                    min(b0 + tid, C::NBLK - 1));
+        return;
+    } else {
 #pragma unroll 1
-        for (int b0 = 0; b0 < C::NBLK; b0 += NT) {
-            if constexpr (P2)
-                forward_block_p2<C, MS, RF, BATCH_ROWS>(p, sU, phif, k, tb, min(b0 + tid, C::NBLK - 1));
-            else
-                forward_block<C, MS, RF, FAST, BATCH_ROWS, true>(p, sU, phif, k, tb, tabf, min(b0 + tid, C::NBLK - 1));
+        for (int fi = 0; fi < F; ++fi) {
+            const float* k = kg + fi * TL::per_filter;
+            const float* tabf = tabg + fi * p.tab3_stride;
+            const uint32_t tb = static_cast<uint32_t>(__cvta_generic_to_shared(tabf)) + p.tab3_bias;
+            float* phif = sPhi + fi * C::SPHI;
+            // warp-uniform control flow (the uniform datapath is only used
+            // outside divergent branches): threads past the last block
+            // recompute it and store the same values
+#pragma unroll 1
+            for (int b0 = 0; b0 < C::NBLK; b0 += NT) {
+                if constexpr (TM == 1)
+                    forward_block_p2<C, MS, RF, BATCH_ROWS>(p, sU, phif, k, tb, min(b0 + tid, C::NBLK - 1));
+                else
+                    forward_block<C, MS, RF, FAST, BATCH_ROWS, true>(p, sU, phif, k, tb, tabf,
+                                                                     min(b0 + tid, C::NBLK - 1));
+            }
         }
     }
 }
@@ -809,16 +913,17 @@ struct ForceAcc {
 // written with pointer increments and a __syncwarp, the form in which ptxas
 // keeps the taps in uniform registers (a plain indexed unroll-1 loop loads
 // them into per-thread registers with LDC)
-template <class C, int MS, int RB, int F, bool P2>
+template <class C, int MS, int RB, int F, int TM>
 __device__ __forceinline__ void backward_group_pt(const float* sPhi, const float* kg, int ox0, int oy0,
-                                                  ForceAcc<MS, RB, P2>& acc) {
+                                                  ForceAcc<MS, RB, (TM == 1 || TM == 2)>& acc) {
     static_assert(C::NSPLIT == 1, "parameter-space taps need one thread per output block");
-    constexpr int KS = P2 ? PairTaps<MS>::kFloats : C::KP;
-    const float* k = kg;
+    using TL = TapLayout<MS, C::KP, F, TM>;
+    const float* k = kg + TL::bwd0;
     const float* ph = sPhi;
 #pragma unroll 1
-    for (int fi = 0; fi < F; ++fi, k += KS, ph += C::SPHI) {
-        if constexpr (P2) backward_filter_p2<C, MS, RB>(ph, k, ox0, oy0, acc.f2);
+    for (int fi = 0; fi < F; ++fi, k += TL::per_filter, ph += C::SPHI) {
+        if constexpr (TM == 1 || TM == 2) backward_filter_p2<C, MS, RB>(ph, k, ox0, oy0, acc.f2);
+        else if constexpr (TM == 3) backward_filter<C, MS, RB>(ph, FpTap<MS>{k}, ox0, oy0, acc.f1);
         else backward_filter<C, MS, RB>(ph, k, ox0, oy0, acc.f1);
         __syncwarp();
     }
@@ -944,7 +1049,7 @@ __device__ __forceinline__ void tbar_wait(uint64_t* bar, uint32_t parity) {
 // ---- tile kernel: one CTA = one output tile, all filter groups -------------
 // PT: taps read from the parameter space (`kp` = this stage's TapBlock)
 // instead of being staged in shared memory and held in registers
-template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, bool PT, bool P2 = false>
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, bool PT, int TM = 0>
 __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float* kp) {
     using C = StageCfg<MS, TH, TW, RF, RB, NT, F>;
     constexpr int R = C::R;
@@ -984,9 +1089,9 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
     const int split = PT ? 0 : tid / (C::OBX * C::OBY);  // which filters of a group
     const int obx = tid % C::OBX, oby = (tid / C::OBX) % C::OBY;
     const int ox0 = obx * 4, oy0 = oby * RB;
-    constexpr int KS = P2 ? PairTaps<MS>::kFloats : C::KP;   // PT tap floats per filter
+    constexpr int GS = TapLayout<MS, C::KP, F, TM>::group;   // PT tap floats per filter group
     float force[RB][4];
-    ForceAcc<MS, RB, P2> facc;   // PT: FFMA2 row pairs (P2) or scalars
+    ForceAcc<MS, RB, (TM == 1 || TM == 2)> facc;   // PT: FFMA2 row pairs (TM 1, 2) or scalars
 #pragma unroll
     for (int r = 0; r < RB; ++r)
 #pragma unroll
@@ -1000,16 +1105,16 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
         __syncthreads();  // params of group g landed; previous bwd done with sPhi
         if constexpr (!PT)
             if (g + 1 < p.ngroups) prefetch_group<C, F, NT>(p, sTap, sTab, g + 1, buf ^ 1, tid);
-        const float* tapg = PT ? kp + g * F * KS : sTap + buf * F * C::KP;
+        const float* tapg = PT ? kp + g * GS : sTap + buf * F * C::KP;
         const float* tabg = sTab + buf * tabsz;
-        if constexpr (PT) forward_group_pt<C, MS, RF, F, NT, FAST, P2>(p, sU, sPhi, tapg, tabg, tid);
+        if constexpr (PT) forward_group_pt<C, MS, RF, F, NT, FAST, TM>(p, sU, sPhi, tapg, tabg, tid);
         else forward_group<C, MS, RF, F, FAST>(p, sU, sPhi, tapg, tabg, tid);
         __syncthreads();
         // PT: the table is free -- fetch the next group's under fix-up + backward
         if constexpr (PT)
             if (tid == 0 && g + 1 < p.ngroups) tbar_fetch(sTab, p.tab3 + (size_t)(g + 1) * tabsz, tabsz, &tbar);
         fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
-        if constexpr (PT) backward_group_pt<C, MS, RB, F, P2>(sPhi, tapg, ox0, oy0, facc);
+        if constexpr (PT) backward_group_pt<C, MS, RB, F, TM>(sPhi, tapg, ox0, oy0, facc);
         else backward_group<C, MS, RB, F>(sPhi, tapg, split, ox0, oy0, force);
     }
     if constexpr (PT) {
@@ -1052,9 +1157,9 @@ struct TapBlock {
     float k[N];
 };
 
-template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB, class TB, bool P2>
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB, class TB, int TM>
 __global__ void __launch_bounds__(NT, MINB) stage_kernel_pt(const StageArgs p, const __grid_constant__ TB tk) {
-    stage_tile_body<MS, TH, TW, RF, RB, NT, FAST, F, true, P2>(p, tk.k);
+    stage_tile_body<MS, TH, TW, RF, RB, NT, FAST, F, true, TM>(p, tk.k);
 }
 
 // ---- split kernels: work units = (tile, filter group) ----------------------
@@ -1173,7 +1278,7 @@ __device__ __forceinline__ void stage_split_body(const StageArgs& p, const Split
 // order, walked as tile segments (u staged in the outer loop) so that the
 // inner group loop holds only shared-memory traffic and the partial store:
 // ptxas then keeps the group index -- and the tap addresses -- uniform.
-template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, bool P2>
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int TM>
 __device__ __forceinline__ void stage_split_body_pt(const StageArgs& p, const SplitWs& ws, const float* kp) {
     using C = StageCfg<MS, TH, TW, RF, RB, NT, F>;
     constexpr int TPX = TH * TW;
@@ -1217,19 +1322,19 @@ __device__ __forceinline__ void stage_split_body_pt(const StageArgs& p, const Sp
         for (int g = g0; g < gend; ++g, ++k) {
             tbar_wait(&tbar, k & 1);
             __syncthreads();  // table + u tile in smem; previous unit done with sPhi
-            const float* tapg = kp + g * F * (P2 ? PairTaps<MS>::kFloats : C::KP);
+            const float* tapg = kp + g * TapLayout<MS, C::KP, F, TM>::group;
             const float* tabg = sTab;
             // all RF rows' table lookups before the phi stores (with the taps
             // out of the registers this pays here too: +1% C2 on B200)
-            forward_group_pt<C, MS, RF, F, NT, FAST, P2>(p, sU, sPhi, tapg, tabg, tid);
+            forward_group_pt<C, MS, RF, F, NT, FAST, TM>(p, sU, sPhi, tapg, tabg, tid);
             __syncthreads();
             // the table is free: fetch the next unit's under fix-up + backward
             if (tid == 0 && k + 1 < nunits)
                 tbar_fetch(sTab, p.tab3 + (size_t)(g + 1 < ng ? g + 1 : 0) * tabsz, tabsz, &tbar);
             fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
-            ForceAcc<MS, RB, P2> facc;
+            ForceAcc<MS, RB, (TM == 1 || TM == 2)> facc;
             facc.zero();
-            backward_group_pt<C, MS, RB, F, P2>(sPhi, tapg, ox0, oy0, facc);
+            backward_group_pt<C, MS, RB, F, TM>(sPhi, tapg, ox0, oy0, facc);
 #pragma unroll
             for (int r = 0; r < RB; ++r)
                 __stcg(reinterpret_cast<float4*>(dst + (size_t)g * TPX + r * TW),
@@ -1243,10 +1348,10 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel_split(const StageArgs p
     stage_split_body<MS, TH, TW, RF, RB, NT, FAST, F>(p, ws);
 }
 
-template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB, class TB, bool P2>
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB, class TB, int TM>
 __global__ void __launch_bounds__(NT, MINB) stage_kernel_split_pt(const StageArgs p, const SplitWs ws,
                                                                  const __grid_constant__ TB tk) {
-    stage_split_body_pt<MS, TH, TW, RF, RB, NT, FAST, F, P2>(p, ws, tk.k);
+    stage_split_body_pt<MS, TH, TW, RF, RB, NT, FAST, F, TM>(p, ws, tk.k);
 }
 
 // sum of a pixel quad's partials in group order, then the epilogue (u from
