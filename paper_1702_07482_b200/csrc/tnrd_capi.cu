@@ -634,6 +634,19 @@ struct SplitTile {
 
 
 constexpr size_t kMaxSplitBytes = size_t(1) << 30;
+// split workspace: the range-claim control words (fixed place: they must
+// stay zeroed whatever partial sizes later launches write), then the partial
+// forces
+constexpr size_t kSplitCtlBytes = (kSplitCtlWords * sizeof(uint32_t) + 255) / 256 * 256;
+static size_t split_alloc_bytes(size_t part_bytes) { return kSplitCtlBytes + part_bytes; }
+// SM-aware split ranges (tnrd_stage.cuh SplitWs): measured on B200 slower
+// than blockIdx ranges although it removes the 12-unit SMs (C2 636 ->
+// 606 / 595 MPix/s with the heavy ranges on the first / last CTA of an SM,
+// profiles/r02_split_map), so off by default
+#ifndef TNRD_SPLIT_MAP
+#define TNRD_SPLIT_MAP 0
+#endif
+constexpr bool kMapSplit = TNRD_SPLIT_MAP != 0;
 static int sm_count();
 
 #ifdef TNRD_EXPERIMENTS
@@ -994,9 +1007,14 @@ struct StageKernel {
         w.tiles_x = (a.W + TW - 1) / TW;
         w.tiles_y = (a.H + TH - 1) / TH;
         w.tiles = w.tiles_x * w.tiles_y * batch;
-        w.part = static_cast<float*>(wsp);
+        w.part = reinterpret_cast<float*>(static_cast<char*>(wsp) + kSplitCtlBytes);
         const long units = (long)w.tiles * b.ngroups;
         const int grid = (int)std::min<long>(units, (long)sms * per_sm);
+        // SM-aware ranges (tnrd_stage.cuh SplitWs) for the parameter-space
+        // kernel when the grid is whole SMs x resident CTAs
+        w.ctl = static_cast<uint32_t*>(wsp);
+        w.map_sms = (kMapSplit && sizeof...(extra) > 0 && grid % sms == 0 && sms <= kSplitCtlSms &&
+                     grid <= kSplitCtlRanges) ? sms : 0;
         CUDA_TRY(launch_pdl(kern, grid, NT, smem, s, b, w, extra...));
         const long quads = (long)w.tiles * (TH * TW / 4);
         const int rgrid = (int)std::min<long>((quads + 127) / 128, (long)sms * 16);
@@ -1078,9 +1096,10 @@ static int dispatch_split_m_t(int m, const StageArgs& a, int batch, void* ws, cu
 }
 
 // the stream's split workspace, grown on demand (outside stream capture)
-static int split_workspace(const tnrd_model* md, cudaStream_t s, size_t bytes, void** out) {
+static int split_workspace(const tnrd_model* md, cudaStream_t s, size_t part_bytes, void** out) {
     std::lock_guard<std::mutex> lk(md->ws_mu);
     auto& b = md->ws[s];
+    const size_t bytes = split_alloc_bytes(part_bytes);
     if (b.bytes < bytes) {
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         CUDA_TRY(cudaStreamIsCapturing(s, &cs));
@@ -1093,6 +1112,10 @@ static int split_workspace(const tnrd_model* md, cudaStream_t s, size_t bytes, v
         }
         CUDA_TRY(cudaMalloc(&b.ptr, bytes));
         b.bytes = bytes;
+        // control words start zeroed (the kernels leave them zeroed); the
+        // partials region may be reused by other sizes, the control words
+        // sit past the largest partials this buffer holds
+        CUDA_TRY(cudaMemsetAsync(b.ptr, 0, bytes, s));
     }
     *out = b.ptr;
     return TNRD_OK;

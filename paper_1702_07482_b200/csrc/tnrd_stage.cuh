@@ -384,6 +384,36 @@ __device__ __forceinline__ void load_taps(const float* tap, float (&k)[C::KK]) {
 // a pointer into the kernel's parameter space (TapBlock: warp-uniform, read
 // by the uniform datapath -- LDCU + FFMA with a uniform-register operand --
 // so the taps hold no per-thread registers).
+// RBF lookups interleaved with the convolution (forward_block, forward_block_fp)
+#ifndef TNRD_FWD_INTERLEAVE
+#define TNRD_FWD_INTERLEAVE 1
+#endif
+
+// phi = rbf(z) of one 4-wide row (cubic table / degree-7 table / direct sum)
+template <bool FAST, bool CUBIC>
+__device__ __forceinline__ float4 rbf_row(const float (&z)[4], uint32_t tb, const float* tabf, const StageArgs& p) {
+    float4 o;
+    if (CUBIC) {
+        o.x = rbf_cubic_s(z[0], tb, p); o.y = rbf_cubic_s(z[1], tb, p);
+        o.z = rbf_cubic_s(z[2], tb, p); o.w = rbf_cubic_s(z[3], tb, p);
+    } else if (FAST) {
+        o.x = rbf_poly_s(z[0], tb, p); o.y = rbf_poly_s(z[1], tb, p);
+        o.z = rbf_poly_s(z[2], tb, p); o.w = rbf_poly_s(z[3], tb, p);
+    } else {
+        o.x = rbf_direct(z[0], tabf, p); o.y = rbf_direct(z[1], tabf, p);
+        o.z = rbf_direct(z[2], tabf, p); o.w = rbf_direct(z[3], tabf, p);
+    }
+    return o;
+}
+
+// forward of one RF x 4 phi block of one filter: z = conv(u, k), phi = rbf(z).
+// K is the filter's taps: a register array (taps staged in shared memory) or
+// a pointer into the kernel's parameter space (TapBlock: warp-uniform, read
+// by the uniform datapath -- LDCU + FFMA with a uniform-register operand --
+// so the taps hold no per-thread registers).  TNRD_FWD_INTERLEAVE: each
+// output row's lookups right after its last input row, its store one input
+// row later (see forward_block_fp); else the lookups after the convolution,
+// stored in batches of BATCH_ROWS.
 template <class C, int MS, int RF, bool FAST, int BATCH_ROWS, bool CUBIC = false, class K>
 __device__ __forceinline__ void forward_block(const StageArgs& p, const float* sU, float* phif,
                                               const K& k, uint32_t tb, const float* tabf, int blk) {
@@ -391,11 +421,13 @@ __device__ __forceinline__ void forward_block(const StageArgs& p, const float* s
     const int by = blk / C::NBX;
     const int bx = blk - by * C::NBX;
     const int x0 = bx * 4, y0 = by * RF;
+    float* dst = phif + y0 * C::PW + x0;
     float acc[RF][4];
 #pragma unroll
     for (int r = 0; r < RF; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
+    float4 prev;
 #pragma unroll
     for (int rr = 0; rr < RF + 2 * R; ++rr) {
         float v[4 * C::NV];
@@ -418,37 +450,27 @@ __device__ __forceinline__ void forward_block(const StageArgs& p, const float* s
                 }
             }
         }
-    }
-    float* dst = phif + y0 * C::PW + x0;
-    // BATCH_ROWS = RF: all RF x 4 table lookups before the first phi store
-    // (the lookups are ordered asm loads with a memory clobber, so a
-    // store between rows caps the lookups in flight at one row's four).
-    // Measured on B200: +5% for the tile kernel (C3), -7% for the split
-    // kernel (C2), which therefore stores in smaller row batches.
-    float4 o[RF];
-#pragma unroll
-    for (int r = 0; r < RF; ++r) {
-        if (CUBIC) {
-            o[r].x = rbf_cubic_s(acc[r][0], tb, p);
-            o[r].y = rbf_cubic_s(acc[r][1], tb, p);
-            o[r].z = rbf_cubic_s(acc[r][2], tb, p);
-            o[r].w = rbf_cubic_s(acc[r][3], tb, p);
-        } else if (FAST) {
-            o[r].x = rbf_poly_s(acc[r][0], tb, p);
-            o[r].y = rbf_poly_s(acc[r][1], tb, p);
-            o[r].z = rbf_poly_s(acc[r][2], tb, p);
-            o[r].w = rbf_poly_s(acc[r][3], tb, p);
-        } else {
-            o[r].x = rbf_direct(acc[r][0], tabf, p);
-            o[r].y = rbf_direct(acc[r][1], tabf, p);
-            o[r].z = rbf_direct(acc[r][2], tabf, p);
-            o[r].w = rbf_direct(acc[r][3], tabf, p);
+        if constexpr (TNRD_FWD_INTERLEAVE) {
+            const int r = rr - 2 * R;   // output row completed by this input row
+            if (r >= 1) *reinterpret_cast<float4*>(dst + (r - 1) * C::PW) = prev;
+            if (r >= 0) prev = rbf_row<FAST, CUBIC>(acc[r], tb, tabf, p);
         }
-        // store rows in batches of BATCH_ROWS (all RF rows: one batch)
-        if ((r + 1) % BATCH_ROWS == 0 || r == RF - 1) {
+    }
+    if constexpr (TNRD_FWD_INTERLEAVE) {
+        *reinterpret_cast<float4*>(dst + (RF - 1) * C::PW) = prev;
+    } else {
+        // BATCH_ROWS = RF: all RF x 4 table lookups before the first phi
+        // store (the lookups are ordered asm loads with a memory clobber, so
+        // a store between rows caps the lookups in flight at one row's four)
+        float4 o[RF];
 #pragma unroll
-            for (int q = r - (r % BATCH_ROWS); q <= r; ++q)
-                *reinterpret_cast<float4*>(dst + q * C::PW) = o[q];
+        for (int r = 0; r < RF; ++r) {
+            o[r] = rbf_row<FAST, CUBIC>(acc[r], tb, tabf, p);
+            if ((r + 1) % BATCH_ROWS == 0 || r == RF - 1) {
+#pragma unroll
+                for (int q = r - (r % BATCH_ROWS); q <= r; ++q)
+                    *reinterpret_cast<float4*>(dst + q * C::PW) = o[q];
+            }
         }
     }
 }
@@ -548,9 +570,13 @@ struct FpTap {
     __device__ __forceinline__ float operator[](int i) const { return fp[2 * (MS * MS - 1 - i)]; }
 };
 
-// forward of both filters of a group (TM 2): one RF x 4 block, z of filter
-// 0 / 1 in the low / high lane of each FFMA2 (same fma.rn chain per filter as
-// the scalar forward_block, so the same bits)
+// forward of both filters of a group (TM 2, 3): one RF x 4 block, z of
+// filter 0 / 1 in the low / high lane of each FFMA2 (same fma.rn chain per
+// filter as the scalar forward_block, so the same bits).  Output row r is
+// complete after input row r + 2R: with TNRD_FWD_INTERLEAVE its RBF lookups
+// are issued right there and its phi stored one input row later, so the
+// lookup latency hides under the remaining rows' FFMA2s (instead of a
+// lookup-only tail after the convolution).
 template <class C, int MS, int RF, int BATCH_ROWS>
 __device__ __forceinline__ void forward_block_fp(const StageArgs& p, const float* sU, float* phi0, float* phi1,
                                                  const float* kfp, uint32_t tb0, uint32_t tb1, int blk) {
@@ -558,11 +584,14 @@ __device__ __forceinline__ void forward_block_fp(const StageArgs& p, const float
     const int by = blk / C::NBX;
     const int bx = blk - by * C::NBX;
     const int x0 = bx * 4, y0 = by * RF;
+    float* d0 = phi0 + y0 * C::PW + x0;
+    float* d1 = phi1 + y0 * C::PW + x0;
     f2_t acc2[RF][4];
 #pragma unroll
     for (int r = 0; r < RF; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc2[r][c] = 0ull;
+    float4 p0, p1;   // interleave: phi of the previous completed row, stored one row later
 #pragma unroll
     for (int rr = 0; rr < RF + 2 * R; ++rr) {
         float v[4 * C::NV];
@@ -586,25 +615,45 @@ __device__ __forceinline__ void forward_block_fp(const StageArgs& p, const float
                 }
             }
         }
+        if constexpr (TNRD_FWD_INTERLEAVE) {
+            const int r = rr - 2 * R;   // output row completed by this input row
+            if (r >= 1) {
+                *reinterpret_cast<float4*>(d0 + (r - 1) * C::PW) = p0;
+                *reinterpret_cast<float4*>(d1 + (r - 1) * C::PW) = p1;
+            }
+            if (r >= 0) {
+                p0.x = rbf_cubic_s(f2_lo(acc2[r][0]), tb0, p);
+                p0.y = rbf_cubic_s(f2_lo(acc2[r][1]), tb0, p);
+                p0.z = rbf_cubic_s(f2_lo(acc2[r][2]), tb0, p);
+                p0.w = rbf_cubic_s(f2_lo(acc2[r][3]), tb0, p);
+                p1.x = rbf_cubic_s(f2_hi(acc2[r][0]), tb1, p);
+                p1.y = rbf_cubic_s(f2_hi(acc2[r][1]), tb1, p);
+                p1.z = rbf_cubic_s(f2_hi(acc2[r][2]), tb1, p);
+                p1.w = rbf_cubic_s(f2_hi(acc2[r][3]), tb1, p);
+            }
+        }
     }
-    float* d0 = phi0 + y0 * C::PW + x0;
-    float* d1 = phi1 + y0 * C::PW + x0;
-    float4 o0[RF], o1[RF];
+    if constexpr (TNRD_FWD_INTERLEAVE) {
+        *reinterpret_cast<float4*>(d0 + (RF - 1) * C::PW) = p0;
+        *reinterpret_cast<float4*>(d1 + (RF - 1) * C::PW) = p1;
+    } else {
+        float4 o0[RF], o1[RF];
 #pragma unroll
-    for (int r = 0; r < RF; ++r) {
-        o0[r].x = rbf_cubic_s(f2_lo(acc2[r][0]), tb0, p);
-        o0[r].y = rbf_cubic_s(f2_lo(acc2[r][1]), tb0, p);
-        o0[r].z = rbf_cubic_s(f2_lo(acc2[r][2]), tb0, p);
-        o0[r].w = rbf_cubic_s(f2_lo(acc2[r][3]), tb0, p);
-        o1[r].x = rbf_cubic_s(f2_hi(acc2[r][0]), tb1, p);
-        o1[r].y = rbf_cubic_s(f2_hi(acc2[r][1]), tb1, p);
-        o1[r].z = rbf_cubic_s(f2_hi(acc2[r][2]), tb1, p);
-        o1[r].w = rbf_cubic_s(f2_hi(acc2[r][3]), tb1, p);
-        if ((r + 1) % BATCH_ROWS == 0 || r == RF - 1) {
+        for (int r = 0; r < RF; ++r) {
+            o0[r].x = rbf_cubic_s(f2_lo(acc2[r][0]), tb0, p);
+            o0[r].y = rbf_cubic_s(f2_lo(acc2[r][1]), tb0, p);
+            o0[r].z = rbf_cubic_s(f2_lo(acc2[r][2]), tb0, p);
+            o0[r].w = rbf_cubic_s(f2_lo(acc2[r][3]), tb0, p);
+            o1[r].x = rbf_cubic_s(f2_hi(acc2[r][0]), tb1, p);
+            o1[r].y = rbf_cubic_s(f2_hi(acc2[r][1]), tb1, p);
+            o1[r].z = rbf_cubic_s(f2_hi(acc2[r][2]), tb1, p);
+            o1[r].w = rbf_cubic_s(f2_hi(acc2[r][3]), tb1, p);
+            if ((r + 1) % BATCH_ROWS == 0 || r == RF - 1) {
 #pragma unroll
-            for (int q = r - (r % BATCH_ROWS); q <= r; ++q) {
-                *reinterpret_cast<float4*>(d0 + q * C::PW) = o0[q];
-                *reinterpret_cast<float4*>(d1 + q * C::PW) = o1[q];
+                for (int q = r - (r % BATCH_ROWS); q <= r; ++q) {
+                    *reinterpret_cast<float4*>(d0 + q * C::PW) = o0[q];
+                    *reinterpret_cast<float4*>(d1 + q * C::PW) = o1[q];
+                }
             }
         }
     }
@@ -1184,7 +1233,70 @@ __global__ void __launch_bounds__(NT, MINB) stage_kernel_pt(const StageArgs p, c
 struct SplitWs {
     float* part;       // [tiles][ngroups][TH*TW] partial forces
     int tiles_x, tiles_y, tiles;
+    // SM-aware range assignment of the parameter-space split kernel (0 = off:
+    // CTA c takes range c).  With the grid = map_sms x P resident CTAs, the
+    // k-th CTA to arrive on SM s (k < P) takes range k * map_sms + s, so
+    // the ranges that carry one extra unit (the first units % grid) land on
+    // distinct SMs; measured on B200 the block scheduler otherwise pairs two
+    // of them on one SM (12 units there instead of 11).  Ranges are claimed
+    // with a CAS on `ctl`, and a CTA that arrives as a third on its SM (the
+    // SMs were shared with another kernel) takes any unclaimed range, so
+    // every range runs exactly once whatever the placement.  The last CTA to
+    // finish zeroes `ctl` for the next launch on this workspace.
+    uint32_t* ctl;     // [kSplitCtlSms] per-SM arrivals | [kSplitCtlRanges] claimed | count | done
+    int map_sms;
 };
+constexpr int kSplitCtlSms = 256;
+constexpr int kSplitCtlRanges = 4096;
+constexpr size_t kSplitCtlWords = kSplitCtlSms + kSplitCtlRanges + 2;
+
+// thread 0: claim an unclaimed range (lowest first); -1 when all are taken
+__device__ __forceinline__ int split_claim_any(const SplitWs& ws) {
+    uint32_t* claimed = ws.ctl + kSplitCtlSms;
+    uint32_t* count = claimed + kSplitCtlRanges;
+    for (int c = 0; c < (int)gridDim.x; ++c) {
+        if (atomicAdd(count, 0u) >= gridDim.x) return -1;
+        if (atomicCAS(claimed + c, 0u, 1u) == 0u) {
+            atomicAdd(count, 1u);
+            return c;
+        }
+    }
+    return -1;
+}
+// thread 0: this CTA's first range (SM-aware when ws.map_sms > 0)
+__device__ __forceinline__ int split_claim_first(const SplitWs& ws) {
+    if (ws.map_sms <= 0) return blockIdx.x;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if ((int)smid < ws.map_sms && (int)smid < kSplitCtlSms) {
+        const uint32_t k = atomicAdd(ws.ctl + smid, 1u);
+        const uint32_t P = gridDim.x / (uint32_t)ws.map_sms;
+        // the LAST CTA to arrive on an SM takes the lowest range (the ranges
+        // with the extra unit): its warps have the higher slots, which the
+        // warp arbiter issues first (measured: the earlier CTA of an SM
+        // finishes its share later)
+        const int c = (int)(P - 1 - k) * ws.map_sms + (int)smid;
+        if (k < P && c < (int)gridDim.x && atomicCAS(ws.ctl + kSplitCtlSms + c, 0u, 1u) == 0u) {
+            atomicAdd(ws.ctl + kSplitCtlSms + kSplitCtlRanges, 1u);
+            return c;
+        }
+    }
+    return split_claim_any(ws);
+}
+// thread 0, after the CTA's last range: the last CTA of the launch resets ctl
+__device__ __forceinline__ void split_finish(const SplitWs& ws) {
+    if (ws.map_sms <= 0) return;
+    __threadfence();
+    uint32_t* done = ws.ctl + kSplitCtlSms + kSplitCtlRanges + 1;
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+        __threadfence();
+        for (int i = 0; i < kSplitCtlSms; ++i) ws.ctl[i] = 0u;
+        for (int i = 0; i < (int)gridDim.x && i < kSplitCtlRanges; ++i) ws.ctl[kSplitCtlSms + i] = 0u;
+        ws.ctl[kSplitCtlSms + kSplitCtlRanges] = 0u;
+        *done = 0u;
+        __threadfence();
+    }
+}
 
 #ifdef TNRD_SPLIT_TRACE
 // per-CTA timeline for tools/split_trace.py: smid, t0, t1, units | first << 32
@@ -1294,21 +1406,39 @@ __device__ __forceinline__ void stage_split_body_pt(const StageArgs& p, const Sp
 
     const int units = ws.tiles * ng;
     const int nb = units / (int)gridDim.x, extra = units % (int)gridDim.x;
-    const int c = blockIdx.x;
-    const int ubeg = c * nb + min(c, extra);
-    const int nunits = nb + (c < extra ? 1 : 0);
     const int obx = tid % C::OBX, oby = tid / C::OBX;
     const int ox0 = obx * 4, oy0 = oby * RB;
 
     __shared__ __align__(8) uint64_t tbar;  // the table buffer's fills
+    __shared__ int s_range;                 // range being processed (-1: none left)
     if (tid == 0) {
         tbar_init(&tbar);
-        if (nunits > 0) tbar_fetch(sTab, p.tab3 + (size_t)(ubeg % ng) * tabsz, tabsz, &tbar);
+        // the ranges' control words are not written by the previous grid,
+        // so the claim may run before the dependency wait
+        const int c = split_claim_first(ws);
+        s_range = c;
+        if (c >= 0 && nb + (c < extra ? 1 : 0) > 0)
+            tbar_fetch(sTab, p.tab3 + (size_t)((c * nb + min(c, extra)) % ng) * tabsz, tabsz, &tbar);
     }
     __syncthreads();  // barrier initialised before anyone waits
     pdl_wait();       // the previous stage wrote u_in
     pdl_trigger();    // the reduction may be scheduled as CTAs retire
-    int k = 0;        // units done (= table fills completed)
+#ifdef TNRD_SPLIT_TRACE
+    const unsigned long long tr_t0 = gtimer();
+    int ubeg = 0, nunits = 0;
+#endif
+    uint32_t fills = 0;   // table fills consumed before this range (mbarrier parity)
+  for (;;) {
+    const int c = s_range;
+    if (c < 0) break;
+#ifndef TNRD_SPLIT_TRACE
+    const int ubeg = c * nb + min(c, extra);
+    const int nunits = nb + (c < extra ? 1 : 0);
+#else
+    ubeg = c * nb + min(c, extra);
+    nunits = nb + (c < extra ? 1 : 0);
+#endif
+    int k = 0;        // units done in this range (= table fills completed)
     while (k < nunits) {
         const int unit = ubeg + k;
         const int tile = unit / ng, g0 = unit - tile * ng;
@@ -1320,7 +1450,7 @@ __device__ __forceinline__ void stage_split_body_pt(const StageArgs& p, const Sp
         stage_u_tile<C, NT>(p, sU, p.u_in + (int64_t)img * p.img_stride, Y0, X0, top_halo, bot_halo, tid);
         float* dst = ws.part + (size_t)tile * ng * TPX + oy0 * TW + ox0;
         for (int g = g0; g < gend; ++g, ++k) {
-            tbar_wait(&tbar, k & 1);
+            tbar_wait(&tbar, (fills + k) & 1);
             __syncthreads();  // table + u tile in smem; previous unit done with sPhi
             const float* tapg = kp + g * TapLayout<MS, C::KP, F, TM>::group;
             const float* tabg = sTab;
@@ -1341,6 +1471,27 @@ __device__ __forceinline__ void stage_split_body_pt(const StageArgs& p, const Sp
                        make_float4(facc.get(r, 0), facc.get(r, 1), facc.get(r, 2), facc.get(r, 3)));
         }
     }
+    fills += nunits;
+    __syncthreads();  // every thread has read s_range and is done with sTab
+    if (tid == 0) {
+        const int c2 = ws.map_sms > 0 ? split_claim_any(ws) : -1;
+        s_range = c2;
+        if (c2 >= 0 && nb + (c2 < extra ? 1 : 0) > 0)
+            tbar_fetch(sTab, p.tab3 + (size_t)((c2 * nb + min(c2, extra)) % ng) * tabsz, tabsz, &tbar);
+    }
+    __syncthreads();
+  }
+    if (tid == 0) split_finish(ws);
+#ifdef TNRD_SPLIT_TRACE
+    if (tid == 0 && blockIdx.x < 4096) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_split_trace[blockIdx.x][0] = smid;
+        g_split_trace[blockIdx.x][1] = tr_t0;
+        g_split_trace[blockIdx.x][2] = gtimer();
+        g_split_trace[blockIdx.x][3] = (unsigned long long)nunits | ((unsigned long long)(unsigned)ubeg << 32);
+    }
+#endif
 }
 
 template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB>
