@@ -700,7 +700,13 @@ def main():
     if forked and stage_kernels == 2:
         stage_kernels = "stage_kernel_pt (fused tile kernel) x 2 batch halves on two streams"
     else:
-        stage_kernels = {1: "stage_kernel_pt (fused tile kernel)",
+        tiles_rank = -(-H // 64) * -(-W // 64) * (px_rank // (H * W))
+        one = ("stage_kernel_pt (fused tile kernel)" if tiles_rank >= 2 * 3 * 2 * sms else
+               "stage_kernel_cl_pt (fused cluster kernel: a tile's filter groups on the CTAs of a "
+               "thread-block cluster, partial forces summed through distributed shared memory)")
+        if cfg.name == "c1":
+            one = one.replace("stage_kernel_cl_pt", "stage_kernel_cl")
+        stage_kernels = {1: one,
                          2: "stage_kernel_split_pt + stage_reduce_kernel"}.get(stage_kernels,
                                                                                  str(stage_kernels))
     px_launch = px_rank

@@ -122,10 +122,22 @@ int tnrd_model_rbf_fit_cubic(const tnrd_model* model, double* max_abs_err,
  * CUDA-core RBF + adjoint + prox kernel; m <= 7, nk <= 128), 9 = fused dataflow despeckle (all stages of
  * tnrd_despeckle in one persistent launch, tiles of stage t+1 started as
  * their neighbourhood of stage t is reduced; opt-in, measured slower on
- * B200 than the per-stage split kernel).  Auto runs the split kernel on grids below
- * 3 waves of large tiles; it keeps a partial-force workspace per stream
- * inside the model (allocated on first use, outside stream capture). */
+ * B200 than the per-stage split kernel), 10 / 11 = cluster kernel with
+ * large / small tiles forced: ONE launch per stage on small grids -- the
+ * CTAs of a thread-block cluster split a tile's filter groups, keep their
+ * partial forces in shared memory and sum them in rank order through
+ * distributed shared memory, each CTA finishing its share of the tile's
+ * pixels (diffusion_step, diffusion.py:184-194, as one operator).  Auto
+ * runs the split kernel on grids below 3 waves of large tiles; it keeps a
+ * partial-force workspace per stream inside the model (allocated on first
+ * use, outside stream capture). */
 int tnrd_set_stage_kernel(int mode);
+/* CTAs per cluster of the cluster kernel: 0 = chosen from the grid size
+ * (the largest cluster <= 8 whose CTAs fit one wave), 2..8 = forced.  The
+ * partial forces are summed in cluster-rank order, so results are
+ * bit-reproducible for a given cluster size and differ between sizes by
+ * fp32 summation order only. */
+int tnrd_set_cluster_size(int ctas);
 /* Where the CUDA-core large-tile stage kernels read the filter taps
  * (process-wide): 1 (default) = the kernel parameter space, read by the
  * uniform datapath (m <= 7, nk <= 48 with m = 7); 0 = staged in shared memory

@@ -56,6 +56,7 @@ SIGNATURES = {
                                     ctypes.POINTER(_c_int)]),
     "tnrd_set_stage_kernel": (_c_int, [_c_int]),
     "tnrd_set_param_taps": (_c_int, [_c_int]),
+    "tnrd_set_cluster_size": (_c_int, [_c_int]),
     "tnrd_set_zfield_passes": (_c_int, [_c_int]),
     "tnrd_status_reset": (_c_int, [_vp, _vp]),
     "tnrd_status_decode": (_c_int, [ctypes.POINTER(_c_u32),
@@ -154,12 +155,19 @@ KERNEL_SMALL_TILES, KERNEL_LARGE_TILES = 3, 4
 KERNEL_TC_PHASED = 5
 KERNEL_SPLIT_LARGE, KERNEL_SPLIT_SMALL = 6, 7
 KERNEL_ZFIELD = 8
+KERNEL_CLUSTER_LARGE, KERNEL_CLUSTER_SMALL = 10, 11
 
 
 def set_stage_kernel(mode: int) -> None:
     """0 auto, 1 CUDA-core, 2 tcgen05 forward GEMM, 3/4 CUDA-core with
     small/large tiles forced."""
     check(load().tnrd_set_stage_kernel(int(mode)))
+
+
+def set_cluster_size(ctas: int) -> None:
+    """CTAs per cluster of the cluster kernels (modes 10 / 11 and auto on
+    small grids): 0 = from the grid size, 2..8 forced."""
+    check(load().tnrd_set_cluster_size(int(ctas)))
 
 
 def set_param_taps(on: bool) -> None:

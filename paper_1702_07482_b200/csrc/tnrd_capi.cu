@@ -86,6 +86,16 @@ extern "C" uint32_t tnrd_build_features(void) {
 #endif
 }
 extern "C" void tnrd_launch_count_reset(void) { g_launches.store(0); }
+#ifdef TNRD_PHASE_TRACE
+// tools/phase_trace.py: read (and clear) the tile kernel's per-phase clocks
+extern "C" __attribute__((visibility("default"))) int tnrd_phase_trace(unsigned long long* out8) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpyFromSymbol(out8, g_phase, 8 * sizeof(unsigned long long)));
+    unsigned long long z[8] = {0};
+    CUDA_TRY(cudaMemcpyToSymbol(g_phase, z, sizeof(z)));
+    return TNRD_OK;
+}
+#endif
 
 // ----------------------------------------------------------------- model
 
@@ -151,7 +161,10 @@ struct tnrd_model {
 // 6 / 7 = CUDA-core split kernel with large / small tiles forced (one
 // launch pair per stage), 9 = fused dataflow despeckle (tnrd_despeckle /
 // plans: all stages in one launch; opt-in), 8 = z-field stage
-// (tnrd_stage_zf.cuh: tcgen05 forward over the image + TMA-fed RBF/adjoint)
+// (tnrd_stage_zf.cuh: tcgen05 forward over the image + TMA-fed RBF/adjoint),
+// 10 / 11 = cluster kernel (one launch per stage: a tile's filter groups on
+// the CTAs of a thread-block cluster, partial forces summed through
+// distributed shared memory) with large / small tiles forced
 static std::atomic<int> g_kernel_mode{0};
 // tnrd_set_param_taps; -1 = not set (TNRD_PARAM_TAPS=0|1 gives the initial value)
 static std::atomic<int> g_param_taps{-1};
@@ -162,8 +175,18 @@ extern "C" int tnrd_set_param_taps(int on) {
 }
 
 extern "C" int tnrd_set_stage_kernel(int mode) {
-    if (mode < 0 || mode > 9) return fail(TNRD_EINVAL, "stage kernel mode must be in 0..9");
+    if (mode < 0 || mode > 11) return fail(TNRD_EINVAL, "stage kernel mode must be in 0..11");
     g_kernel_mode.store(mode);
+    return TNRD_OK;
+}
+
+// CTAs per cluster of the cluster kernels: 0 = by grid size (cluster_size()),
+// 2..8 forced (the summation order, and with it the bits, depends on it)
+static std::atomic<int> g_cluster_size{0};
+extern "C" int tnrd_set_cluster_size(int ctas) {
+    if (ctas != 0 && (ctas < 2 || ctas > kMaxCluster))
+        return fail(TNRD_EINVAL, "cluster size must be 0 (auto) or 2..%d", kMaxCluster);
+    g_cluster_size.store(ctas);
     return TNRD_OK;
 }
 
@@ -593,6 +616,13 @@ extern "C" int tnrd_status_decode(const uint32_t* h, int* bad_stage) {
 #ifndef TNRD_PT_TILE_MINB
 #define TNRD_PT_TILE_MINB 2
 #endif
+// cluster kernel (one launch per stage on small grids): tap layout modes
+#ifndef TNRD_CLUSTER_TM
+#define TNRD_CLUSTER_TM 2
+#endif
+#ifndef TNRD_CLUSTER_TM_M9
+#define TNRD_CLUSTER_TM_M9 3
+#endif
 static bool param_taps_enabled() {
     int v = g_param_taps.load();
     if (v < 0) {
@@ -763,6 +793,27 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, int block, size
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// Same, as thread-block clusters of `cl` CTAs along x (stage_kernel_cl*).
+template <class... KArgs, class... Args>
+static cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, int block, size_t smem, int cl,
+                                      cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = (unsigned)cl;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int MS, bool FAST, class T>
 struct StageKernel {
     static constexpr int TH = T::TH, TW = T::TW, RB = T::RB, NT = T::NT, F = T::F;
@@ -799,6 +850,8 @@ struct StageKernel {
     // C2 -2.5% / +-0 / -1.5%).  All modes give the scalar kernel's bits.
     static constexpr int kTmTile = PairTaps<MS>::kOn ? TNRD_TILE_TM : TNRD_TILE_TM_M9;
     static constexpr int kTmSplit = PairTaps<MS>::kOn ? TNRD_SPLIT_TM : TNRD_SPLIT_TM_M9;
+    // cluster kernel (the tile kernel body, groups split over a cluster)
+    static constexpr int kTmCluster = PairTaps<MS>::kOn ? TNRD_CLUSTER_TM : TNRD_CLUSTER_TM_M9;
     using TB = TapBlock<kMaxParamTaps>;
     // forward blocking (measured on B200): m = 7 RF = 5 (252 blocks per
     // filter for 256 threads); m = 9 RF = 2 (C5 172.5 MPix/s; RF = 3 167.4,
@@ -815,7 +868,8 @@ struct StageKernel {
     static bool pt_fits(const StageArgs& a) {
         return kPT && param_taps_enabled() && a.tab3 != nullptr &&
                tap_floats<kTmTile, F_TILE_PT>(a.nk) <= sizeof(TB) / sizeof(float) &&
-               tap_floats<kTmSplit, F_SPLIT_PT>(a.nk) <= sizeof(TB) / sizeof(float);
+               tap_floats<kTmSplit, F_SPLIT_PT>(a.nk) <= sizeof(TB) / sizeof(float) &&
+               tap_floats<kTmCluster, F_TILE_PT>(a.nk) <= sizeof(TB) / sizeof(float);
     }
     // shared memory of the PT kernels: u | phi[f] | one cubic table for f filters
     template <class CC, int FF>
@@ -854,6 +908,48 @@ struct StageKernel {
                             grp[2 * (a2 * MS + b2) + fi] = k[(MS - 1 - a2) * MS + (MS - 1 - b2)];
             }
         }
+    }
+
+    // one launch per stage as clusters of `cl` CTAs per tile (stage_kernel_cl*:
+    // the cluster's CTAs split the tile's filter groups and sum their partial
+    // forces in rank order through distributed shared memory)
+    static int launch_cluster(const StageArgs& a, int batch, int cl, cudaStream_t s,
+                              const float* htaps = nullptr) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        StageArgs b = a;
+        b.ngroups = (a.nk + F - 1) / F;
+        const dim3 grid(((a.W + TW - 1) / TW) * cl, (a.H + TH - 1) / TH, batch);
+        if constexpr (kPT) {
+            if (htaps && pt_fits(a)) {
+                static std::mutex mu2;
+                static uint64_t attr2 = 0;
+                auto kern = stage_kernel_cl_pt<MS, TH, TW, RF_PT, RB, NT, FAST, F_TILE_PT, TNRD_PT_TILE_MINB, TB, kTmCluster>;
+                int rc = prepare(kern, dev, attr2, mu2);
+                if (rc) return rc;
+                TB tb;
+                fill_taps<kTmCluster, F_TILE_PT>(tb, htaps, a.nk);
+                b.ngroups = (a.nk + F_TILE_PT - 1) / F_TILE_PT;
+                CUDA_TRY(launch_pdl_cluster(kern, grid, NT, pt_smem<CPT, F_TILE_PT>(a), cl, s, b, tb));
+                g_launches.fetch_add(1);
+                return TNRD_OK;
+            }
+        }
+        static std::mutex mu;
+        static uint64_t attr_set = 0;  // per-device bitmask
+        auto kern = stage_kernel_cl<MS, TH, TW, RF, RB, NT, FAST, F, MINB>;
+        int rc = prepare(kern, dev, attr_set, mu);
+        if (rc) return rc;
+        CUDA_TRY(launch_pdl_cluster(kern, grid, NT, C::smem_bytes(a.tab_stride), cl, s, b));
+        g_launches.fetch_add(1);
+        return TNRD_OK;
+    }
+    // filter groups of the cluster kernel for this model (the cluster size
+    // never exceeds it)
+    static int cluster_groups(const StageArgs& a) {
+        if constexpr (kPT)
+            if (pt_fits(a)) return (a.nk + F_TILE_PT - 1) / F_TILE_PT;
+        return (a.nk + F - 1) / F;
     }
 
     static int launch(const StageArgs& a, int batch, cudaStream_t s, const float* htaps = nullptr) {
@@ -1050,15 +1146,75 @@ static bool use_split_large(const StageArgs& a, int batch) {
     return units >= 2L * 2 * sm_count();
 }
 
+// CTAs per cluster for a grid of `tiles` large / small tiles with `groups`
+// filter groups on `slots` resident CTA slots (measured on B200,
+// tools/grid_sweep.py, profiles/r02_cluster): 2 once two CTAs per tile give
+// >= 3.4 waves (finer CTAs only add staging and cluster barriers), else 4
+// while that fills 3/4 of a wave, else the largest cluster (<= 8) that fits
+// one wave.  A forced size (tnrd_set_cluster_size / TNRD_CLUSTER_SIZE) wins.
+static int cluster_size(long tiles, int groups, long slots) {
+    int forced = g_cluster_size.load();
+    if (forced == 0) {
+        static const int env = [] {
+            const char* e = std::getenv("TNRD_CLUSTER_SIZE");
+            const int v = e ? std::atoi(e) : 0;
+            return (v >= 2 && v <= kMaxCluster) ? v : 0;
+        }();
+        forced = env;
+    }
+    groups = std::max(groups, 1);
+    if (forced) return std::min(forced, groups);
+    tiles = std::max(tiles, 1L);
+    long cl;
+    if (10 * 2 * tiles >= 34 * slots) cl = 2;
+    else if (4 * 4 * tiles >= 3 * slots) cl = 4;
+    else cl = std::min<long>(kMaxCluster, std::max<long>(slots / tiles, 2));
+    return (int)std::min<long>(cl, groups);
+}
+
+// Auto mode (measured on B200, profiles/r02_cluster/grid_sweep_*.txt): the
+// tile kernel from 6 waves of large tiles (2 x 3 waves: the batch fork's two
+// halves, or one big scene); below that the cluster kernel -- one launch per
+// stage, a tile's filter groups on 2..8 CTAs -- with large tiles when there
+// are >= 2 (tile, group) units per CTA slot, else small tiles (a 256^2
+// image).  The split kernel (two launches per stage) is no longer chosen
+// (TNRD_AUTO_CLUSTER=0 restores it); a thread-local override pins the
+// variant where two launches must agree bit for bit (the batch fork's
+// halves, the scene bands).
+#ifndef TNRD_AUTO_CLUSTER
+#define TNRD_AUTO_CLUSTER 1
+#endif
+static bool auto_cluster() {
+    static const bool on = [] {
+        const char* e = std::getenv("TNRD_AUTO_CLUSTER");
+        return e ? e[0] != '0' : (TNRD_AUTO_CLUSTER != 0);
+    }();
+    return on;
+}
+static thread_local int t_force_variant = -1;
+struct VariantGuard {
+    int prev;
+    explicit VariantGuard(int v) : prev(t_force_variant) { t_force_variant = v; }
+    ~VariantGuard() { t_force_variant = prev; }
+};
+
 // tile configuration of the CUDA-core stage for this launch: 0 tile kernel
-// small tiles, 1 tile kernel large tiles, 2 split kernel large, 3 split small
+// small tiles, 1 tile kernel large tiles, 2 split kernel large, 3 split
+// small, 4 cluster kernel large tiles, 5 cluster kernel small tiles
 static int cc_variant(const StageArgs& a, int batch) {
     switch (g_kernel_mode.load()) {
         case 3: return 0;
         case 4: return 1;
         case 6: return 2;
         case 7: return 3;
-        default: return use_large_tiles(a, batch) ? 1 : (use_split_large(a, batch) ? 2 : 3);
+        case 10: return 4;
+        case 11: return 5;
+        default:
+            if (t_force_variant >= 0) return t_force_variant;
+            if (!auto_cluster())
+                return use_large_tiles(a, batch) ? 1 : (use_split_large(a, batch) ? 2 : 3);
+            if (StageKernel<7, true, LargeTile>::tiles(a, batch) >= 2 * 3L * 2 * sm_count()) return 1;
+            return use_split_large(a, batch) ? 4 : 5;
     }
 }
 
@@ -1069,6 +1225,23 @@ static int dispatch_m_t(int m, const StageArgs& a, int batch, cudaStream_t s, co
         case 5: return StageKernel<5, FAST, T>::launch(a, batch, s, htaps);
         case 7: return StageKernel<7, FAST, T>::launch(a, batch, s, htaps);
         case 9: return StageKernel<9, FAST, T>::launch(a, batch, s, htaps);
+        default: return fail(TNRD_EUNSUPPORTED, "unsupported filter size %d", m);
+    }
+}
+
+template <bool FAST, class T>
+static int dispatch_cluster_m_t(int m, const StageArgs& a, int batch, long slots_per_sm, cudaStream_t s,
+                                const float* htaps = nullptr) {
+    const long slots = slots_per_sm * sm_count();
+    switch (m) {
+        case 3: { using K = StageKernel<3, FAST, T>;
+                  return K::launch_cluster(a, batch, std::max(2, cluster_size(K::tiles(a, batch), K::cluster_groups(a), slots)), s, htaps); }
+        case 5: { using K = StageKernel<5, FAST, T>;
+                  return K::launch_cluster(a, batch, std::max(2, cluster_size(K::tiles(a, batch), K::cluster_groups(a), slots)), s, htaps); }
+        case 7: { using K = StageKernel<7, FAST, T>;
+                  return K::launch_cluster(a, batch, std::max(2, cluster_size(K::tiles(a, batch), K::cluster_groups(a), slots)), s, htaps); }
+        case 9: { using K = StageKernel<9, FAST, T>;
+                  return K::launch_cluster(a, batch, std::max(2, cluster_size(K::tiles(a, batch), K::cluster_groups(a), slots)), s, htaps); }
         default: return fail(TNRD_EUNSUPPORTED, "unsupported filter size %d", m);
     }
 }
@@ -1128,6 +1301,8 @@ static int dispatch_m(const tnrd_model* md, const StageArgs& a, int batch, cudaS
     const float* htaps = md->h_taps.data() + (size_t)a.stage * md->nk_pad * md->kp;
     if (v == 0) return dispatch_m_t<FAST, SmallTile>(m, a, batch, s);
     if (v == 1) return dispatch_m_t<FAST, LargeTile>(m, a, batch, s, htaps);
+    if (v == 4) return dispatch_cluster_m_t<FAST, LargeTile>(m, a, batch, 2, s, htaps);
+    if (v == 5) return dispatch_cluster_m_t<FAST, SmallTile>(m, a, batch, m >= 9 ? 2 : 3, s);
     // the split kernel's partials workspace is bounded (it only pays off on
     // small grids anyway)
     if ((v == 2 ? split_bytes_m_t<FAST, SplitTile>(m, a, batch)
@@ -1644,7 +1819,7 @@ static const tnrd_model::ForkRes* batch_fork(const tnrd_model* md, int batch, in
     if (s == cudaStreamPerThread) return nullptr;
     StageArgs a = stage_args(md, 0, 0u);
     a.H = H; a.W = W;
-    if (cc_variant(a, batch / 2) != 1) return nullptr;
+    if (!use_large_tiles(a, batch / 2)) return nullptr;   // each half >= 3 waves of the tile kernel
     std::lock_guard<std::mutex> lk(md->ws_mu);
     auto& fr = md->forks[s];
     if (!fr.s2) {
@@ -1686,6 +1861,7 @@ extern "C" int tnrd_despeckle(const tnrd_model* md, const float* f, float* u_out
     // whole batch, so the same bits.  Capture-safe (event fork / join).
     const int b0 = (batch + 1) / 2;
     const int64_t off = (int64_t)b0 * image_stride;
+    VariantGuard vg(1);   // both halves on the large-tile kernel
     CUDA_TRY(cudaEventRecord(fr->fork, s));
     CUDA_TRY(cudaStreamWaitEvent(fr->s2, fr->fork, 0));
     rc = despeckle_stages(md, f, u_out, work, b0, H, W, ld, image_stride, d_status, s);
@@ -1847,6 +2023,8 @@ static int band_count(const tnrd_model* md, int batch, int H, int W) {
     const long tiles_x = (W + LargeTile::TW - 1) / LargeTile::TW;
     const long row_tiles = (H + LargeTile::TH - 1) / LargeTile::TH;
     const long wave3 = 3L * 2 * sm_count();
+    // the whole scene must select the tile kernel in auto mode (cc_variant)
+    if (row_tiles * tiles_x < 2 * wave3) return 0;
     long nb = env ? env : std::min<long>(16, (row_tiles * tiles_x) / wave3);
     nb = std::min(nb, row_tiles);
     return nb >= 2 ? (int)nb : 0;
@@ -1888,6 +2066,7 @@ static int plan_banded_host(tnrd_plan* p, const float* f_host, float* u_host, in
     const tnrd_model* md = p->md;
     int rc = banded_setup(p, nb);
     if (rc) return rc;
+    VariantGuard vg(1);   // every band on the whole scene's kernel (large tiles)
     // work queued earlier on the plan's stream (tnrd_plan_despeckle_device
     // returns without a sync) uses the same buffers: the copy and band
     // streams start after it

@@ -1095,10 +1095,62 @@ __device__ __forceinline__ void tbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+
+// ---- thread-block clusters (one launch per stage on small grids) ----------
+// stage_kernel_cl / stage_kernel_cl_pt run a tile's filter groups on the CTAs
+// of one cluster (rank r takes the r-th of cluster-size contiguous, balanced
+// group ranges), leave each CTA's partial force in its shared memory and sum
+// the partials IN RANK ORDER through distributed shared memory, each CTA
+// finishing 1 / cluster-size of the tile's pixels.
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 128-bit load of the shared-memory word at `addr` (a shared::cta address of
+// this CTA's window) in the CTA of cluster rank `rank`
+__device__ __forceinline__ float4 ld_cluster_f4(uint32_t addr, uint32_t rank) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(addr), "r"(rank));
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(ra)
+                 : "memory");
+    return v;
+}
+constexpr int kMaxCluster = 8;   // portable cluster size limit
+
 // ---- tile kernel: one CTA = one output tile, all filter groups -------------
 // PT: taps read from the parameter space (`kp` = this stage's TapBlock)
 // instead of being staged in shared memory and held in registers
-template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, bool PT, int TM = 0>
+#ifdef TNRD_PHASE_TRACE
+// per-phase CTA clock totals of the tile kernel (tools/phase_trace.py):
+// 0 staging, 1 forward + RBF, 2 phi fix-up + table fetch, 3 backward (to the
+// next group's barrier), 4 epilogue, 5 CTAs
+__device__ unsigned long long g_phase[8];
+#define TNRD_PHASE_MARK(i)                                                     \
+    if (tid == 0) {                                                            \
+        const long long t_ = clock64();                                        \
+        atomicAdd(&g_phase[i], (unsigned long long)(t_ - ph_t));               \
+        ph_t = t_;                                                             \
+    }
+#else
+#define TNRD_PHASE_MARK(i)
+#endif
+
+// CLU: launched as clusters along x; the cluster's CTAs share one tile (see
+// the cluster helpers above)
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, bool PT, int TM = 0, bool CLU = false>
 __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float* kp) {
     using C = StageCfg<MS, TH, TW, RF, RB, NT, F>;
     constexpr int R = C::R;
@@ -1113,7 +1165,11 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
     const int tid = threadIdx.x;
     const int img = blockIdx.z;
     const int Y0 = blockIdx.y * TH;
-    const int X0 = blockIdx.x * TW;
+    const int clr = CLU ? (int)cluster_ctarank() : 0;    // this CTA's share of the groups
+    const int cln = CLU ? (int)cluster_nctarank() : 1;
+    const int X0 = (CLU ? (int)blockIdx.x / cln : (int)blockIdx.x) * TW;
+    const int gbeg = CLU ? (p.ngroups * clr) / cln : 0;
+    const int gend = CLU ? (p.ngroups * (clr + 1)) / cln : p.ngroups;
     const float* __restrict__ uin = p.u_in + (int64_t)img * p.img_stride;
     const float* __restrict__ fin = p.f + (int64_t)img * p.img_stride;
     float* __restrict__ uout = p.u_out + (int64_t)img * p.img_stride;
@@ -1125,14 +1181,18 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
     if constexpr (PT) {
         if (tid == 0) {
             tbar_init(&tbar);
-            tbar_fetch(sTab, p.tab3, tabsz, &tbar);
+            if (gbeg < gend) tbar_fetch(sTab, p.tab3 + (size_t)gbeg * tabsz, tabsz, &tbar);
         }
         __syncthreads();  // barrier initialised before anyone waits
     } else {
-        prefetch_group<C, F, NT>(p, sTap, sTab, 0, 0, tid);
+        if (gbeg < gend) prefetch_group<C, F, NT>(p, sTap, sTab, gbeg, 0, tid);
     }
     pdl_wait();     // the previous stage wrote u_in
     pdl_trigger();
+#ifdef TNRD_PHASE_TRACE
+    long long ph_t = clock64();
+    if (tid == 0) atomicAdd(&g_phase[5], 1ull);
+#endif
     stage_u_tile<C, NT>(p, sU, uin, Y0, X0, top_halo, bot_halo, tid);
 
     const int split = PT ? 0 : tid / (C::OBX * C::OBY);  // which filters of a group
@@ -1147,22 +1207,25 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
         for (int c = 0; c < 4; ++c) force[r][c] = 0.0f;
     if constexpr (PT) facc.zero();
 
-    for (int g = 0; g < p.ngroups; ++g) {
-        const int buf = PT ? 0 : g & 1;
-        if constexpr (PT) tbar_wait(&tbar, g & 1);  // fill g of the one buffer
+    for (int g = gbeg; g < gend; ++g) {
+        const int buf = PT ? 0 : (g - gbeg) & 1;
+        if constexpr (PT) tbar_wait(&tbar, (g - gbeg) & 1);  // fill g - gbeg of the one buffer
         else cp_async_wait_all();
         __syncthreads();  // params of group g landed; previous bwd done with sPhi
+        TNRD_PHASE_MARK(g == gbeg ? 0 : 3)
         if constexpr (!PT)
-            if (g + 1 < p.ngroups) prefetch_group<C, F, NT>(p, sTap, sTab, g + 1, buf ^ 1, tid);
+            if (g + 1 < gend) prefetch_group<C, F, NT>(p, sTap, sTab, g + 1, buf ^ 1, tid);
         const float* tapg = PT ? kp + g * GS : sTap + buf * F * C::KP;
         const float* tabg = sTab + buf * tabsz;
         if constexpr (PT) forward_group_pt<C, MS, RF, F, NT, FAST, TM>(p, sU, sPhi, tapg, tabg, tid);
         else forward_group<C, MS, RF, F, FAST>(p, sU, sPhi, tapg, tabg, tid);
         __syncthreads();
+        TNRD_PHASE_MARK(1)
         // PT: the table is free -- fetch the next group's under fix-up + backward
         if constexpr (PT)
-            if (tid == 0 && g + 1 < p.ngroups) tbar_fetch(sTab, p.tab3 + (size_t)(g + 1) * tabsz, tabsz, &tbar);
+            if (tid == 0 && g + 1 < gend) tbar_fetch(sTab, p.tab3 + (size_t)(g + 1) * tabsz, tabsz, &tbar);
         fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
+        TNRD_PHASE_MARK(2)
         if constexpr (PT) backward_group_pt<C, MS, RB, F, TM>(sPhi, tapg, ox0, oy0, facc);
         else backward_group<C, MS, RB, F>(sPhi, tapg, split, ox0, oy0, force);
     }
@@ -1171,6 +1234,58 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
         for (int r = 0; r < RB; ++r)
 #pragma unroll
             for (int c = 0; c < 4; ++c) force[r][c] = facc.get(r, c);
+    }
+#ifdef TNRD_PHASE_TRACE
+    __syncthreads();
+    TNRD_PHASE_MARK(3)
+#endif
+    if constexpr (CLU) {
+        // partial force of this CTA's groups -> shared memory (past the
+        // scratch of reduce_splits), then the ordered sum over the cluster
+        constexpr int TPX = TH * TW;
+        static_assert(C::NSPLIT * TPX <= F * C::SPHI, "partial force must fit the phi buffers");
+        static_assert(TW % 4 == 0 && (C::SPHI % 4) == 0, "float4 partials");
+        const bool full = reduce_splits<C, RB>(sPhi, split, obx, oby, force);
+        if (C::NSPLIT == 1) __syncthreads();   // everyone is done reading sPhi
+        float* sPart = sPhi + (C::NSPLIT - 1) * TPX;
+        if (full) {
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+                *reinterpret_cast<float4*>(sPart + (oy0 + r) * TW + ox0) =
+                    make_float4(force[r][0], force[r][1], force[r][2], force[r][3]);
+        }
+        cluster_sync_all();   // every CTA's partial is visible cluster-wide
+        constexpr int QUADS = TPX / 4;
+        const int qs = (QUADS + cln - 1) / cln;
+        const int qend = min(QUADS, (clr + 1) * qs);
+        const uint32_t pa = smem_addr(sPart);
+        bool bad = false;
+        uint32_t fbits = 0;
+        for (int q = clr * qs + tid; q < qend; q += NT) {
+            const int y = (4 * q) / TW, x = (4 * q) % TW;
+            float4 v[kMaxCluster];
+#pragma unroll
+            for (int r = 0; r < kMaxCluster; ++r)
+                if (r < cln) v[r] = ld_cluster_f4(pa + 16u * (uint32_t)q, (uint32_t)r);
+            float4 acc = v[0];
+#pragma unroll
+            for (int r = 1; r < kMaxCluster; ++r)
+                if (r < cln) { acc.x += v[r].x; acc.y += v[r].y; acc.z += v[r].z; acc.w += v[r].w; }
+            const int Y = Y0 + y;
+            if (Y >= p.H) continue;
+            const float fa[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int X = X0 + x + c;
+                if (X >= p.W) continue;
+                finish_pixel(p, sU[(y + 2 * R) * C::US + x + c + 2 * R], fa[c], fin, uout,
+                             (int64_t)Y * p.ld + X, bad, fbits, fout);
+            }
+        }
+        report(p, bad, fbits);
+        cluster_sync_all();   // no CTA leaves while a peer may still read its partial
+        TNRD_PHASE_MARK(4)
+        return;
     }
     if (!reduce_splits<C, RB>(sPhi, split, obx, oby, force)) return;
 
@@ -1189,6 +1304,7 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
         }
     }
     report(p, bad, fbits);
+    TNRD_PHASE_MARK(4)
 }
 
 template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB>
@@ -1209,6 +1325,18 @@ struct TapBlock {
 template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB, class TB, int TM>
 __global__ void __launch_bounds__(NT, MINB) stage_kernel_pt(const StageArgs p, const __grid_constant__ TB tk) {
     stage_tile_body<MS, TH, TW, RF, RB, NT, FAST, F, true, TM>(p, tk.k);
+}
+
+// cluster variants (launched with a cluster dimension of 2..8 CTAs along x;
+// grid.x = tiles_x * cluster size): one launch per stage on grids that are
+// too small to fill the SMs with whole-tile CTAs
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB>
+__global__ void __launch_bounds__(NT, MINB) stage_kernel_cl(const StageArgs p) {
+    stage_tile_body<MS, TH, TW, RF, RB, NT, FAST, F, false, 0, true>(p, nullptr);
+}
+template <int MS, int TH, int TW, int RF, int RB, int NT, bool FAST, int F, int MINB, class TB, int TM>
+__global__ void __launch_bounds__(NT, MINB) stage_kernel_cl_pt(const StageArgs p, const __grid_constant__ TB tk) {
+    stage_tile_body<MS, TH, TW, RF, RB, NT, FAST, F, true, TM, true>(p, tk.k);
 }
 
 // ---- split kernels: work units = (tile, filter group) ----------------------

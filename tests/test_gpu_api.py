@@ -277,33 +277,35 @@ def test_prox_known_value_minimizer_and_golden(cuda):
 
 
 def test_launch_counter_counts_stages(cuda):
-    """One launch per stage for the tile kernel; two (units + ordered
-    reduction) for the split kernel that auto picks on small grids."""
+    """One launch per stage: the tile kernel, and the cluster kernel that
+    auto picks on small grids; two (units + ordered reduction) for the split
+    kernel (opt-in)."""
     model = synth.make_model(7, 8, 4, 63, seed=9)
     f = np.random.default_rng(0).uniform(1, 255, (40, 40))
     _lib.launch_count_reset()
     tn.run_diffusion(f, model)
-    assert _lib.launch_count() == 8
-    _lib.set_stage_kernel(_lib.KERNEL_LARGE_TILES)
-    try:
-        _lib.launch_count_reset()
-        tn.run_diffusion(f, model)
-        assert _lib.launch_count() == 4
-    finally:
-        _lib.set_stage_kernel(_lib.KERNEL_AUTO)
+    assert _lib.launch_count() == 4
+    for mode, want in ((_lib.KERNEL_LARGE_TILES, 4), (_lib.KERNEL_SPLIT_SMALL, 8)):
+        _lib.set_stage_kernel(mode)
+        try:
+            _lib.launch_count_reset()
+            tn.run_diffusion(f, model)
+            assert _lib.launch_count() == want
+        finally:
+            _lib.set_stage_kernel(_lib.KERNEL_AUTO)
 
 
 def test_plan_graph_replay_matches_eager(cuda):
     """Plans replay a captured CUDA graph from the second call on: results
     must be bit-identical to the eager first call, errors still reported,
-    and each call still counts its 2T split-kernel launches."""
+    and each call still counts its T cluster-kernel launches."""
     model = synth.make_model(7, 8, 4, 63, seed=21)
     f = np.random.default_rng(4).uniform(1, 255, (37, 45))
     outs = []
     for _ in range(4):
         _lib.launch_count_reset()
         u, _ = tn.run_diffusion(f, model)
-        assert _lib.launch_count() == 8
+        assert _lib.launch_count() == 4
         outs.append(u)
     for u in outs[1:]:
         np.testing.assert_array_equal(u, outs[0])

@@ -14,7 +14,8 @@ from paper_1702_07482_b200 import _lib, synth
 pytestmark = pytest.mark.gpu
 
 # 32 x 512^2: the half (16 images, 1,024 large tiles) is >= 3 waves of 2 CTAs
-# per SM on 148 SMs, so auto forks; 16 images alone do not fork (8-image half)
+# per SM on 148 SMs, so auto forks (both halves on the tile kernel); 16 images
+# alone do not fork (8-image half)
 B, HW = 32, 512
 
 
@@ -40,10 +41,11 @@ def test_fork_bit_identical_to_one_stream(cuda, batch):
     _lib.set_stage_kernel(_lib.KERNEL_LARGE_TILES)
     try:
         one = dm.despeckle(fd)
+        # (a 16-image batch alone selects the cluster kernel in auto mode)
+        halves = torch.cat([dm.despeckle(fd[:B // 2]), dm.despeckle(fd[B // 2:])])
     finally:
         _lib.set_stage_kernel(_lib.KERNEL_AUTO)
     assert torch.equal(forked, one)
-    halves = torch.cat([dm.despeckle(fd[:B // 2]), dm.despeckle(fd[B // 2:])])
     assert torch.equal(forked, halves)
 
 

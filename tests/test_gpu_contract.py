@@ -101,7 +101,7 @@ def test_stage_force_one_launch(cuda, variant):
         _lib.launch_count_reset()
         got_u, got_force = dm.stage_force(1, u, f)
         torch.cuda.synchronize()
-        assert _lib.launch_count() in (1, 2)     # tile kernel, or split + reduction
+        assert _lib.launch_count() == 1           # tile or cluster kernel: one launch
         assert torch.equal(got_u, ref_u)
         assert torch.equal(got_force, ref_force)
 
@@ -116,6 +116,6 @@ def test_diffusion_step_single_pass(cuda):
     tn.diffusion_step(u, f, model.stages[0], model)   # upload
     _lib.launch_count_reset()
     u_next, tr = tn.diffusion_step(u, f, model.stages[0], model)
-    assert _lib.launch_count() <= 2
+    assert _lib.launch_count() == 1
     ref = tn.run_diffusion  # noqa: F841  (API present)
     assert np.all(np.isfinite(tr.u_tilde)) and np.array_equal(tr.u_next, u_next)

@@ -109,9 +109,9 @@ def test_split_kernel_reproducible_and_shape_independent(cuda, mode):
         _lib.set_stage_kernel(_lib.KERNEL_AUTO)
 
 
-def test_auto_small_grid_uses_split_and_matches_tile_kernel(cuda):
-    """A single C2 image (auto: split kernel) agrees with the whole-tile
-    kernel to fp32 summation order and runs 2 launches per stage."""
+def test_auto_small_grid_uses_cluster_kernel_and_matches_tile_kernel(cuda):
+    """A single C2 image (auto: cluster kernel) agrees with the whole-tile
+    kernel to fp32 summation order and runs ONE launch per stage."""
     torch = cuda
     cfg = synth.CONFIGS["c2"]
     model = synth.config_model(cfg)
@@ -120,7 +120,7 @@ def test_auto_small_grid_uses_split_and_matches_tile_kernel(cuda):
     _lib.launch_count_reset()
     a = dm.despeckle(f)
     torch.cuda.synchronize()
-    assert _lib.launch_count() == 2 * cfg.T
+    assert _lib.launch_count() == cfg.T
     _lib.set_stage_kernel(_lib.KERNEL_LARGE_TILES)
     try:
         b = dm.despeckle(f)
