@@ -918,8 +918,16 @@ struct StageKernel {
         int dev = 0;
         cudaGetDevice(&dev);
         StageArgs b = a;
-        b.ngroups = (a.nk + F - 1) / F;
-        const dim3 grid(((a.W + TW - 1) / TW) * cl, (a.H + TH - 1) / TH, batch);
+        const int tiles_x = (a.W + TW - 1) / TW, tiles_y = (a.H + TH - 1) / TH;
+        if ((long)tiles_x * tiles_y > 65535) return fail(TNRD_EUNSUPPORTED, "cluster kernel: too many tiles per image");
+        const dim3 grid(cl, tiles_x * tiles_y, batch);
+        auto set_groups = [&](int ng) {
+            b.ngroups = ng;
+            b.cluster = cl;
+            b.cl_gper = ng / cl;
+            b.cl_gextra = ng % cl;
+            b.cl_tiles_x = tiles_x;
+        };
         if constexpr (kPT) {
             if (htaps && pt_fits(a)) {
                 static std::mutex mu2;
@@ -929,7 +937,7 @@ struct StageKernel {
                 if (rc) return rc;
                 TB tb;
                 fill_taps<kTmCluster, F_TILE_PT>(tb, htaps, a.nk);
-                b.ngroups = (a.nk + F_TILE_PT - 1) / F_TILE_PT;
+                set_groups((a.nk + F_TILE_PT - 1) / F_TILE_PT);
                 CUDA_TRY(launch_pdl_cluster(kern, grid, NT, pt_smem<CPT, F_TILE_PT>(a), cl, s, b, tb));
                 g_launches.fetch_add(1);
                 return TNRD_OK;
@@ -940,6 +948,7 @@ struct StageKernel {
         auto kern = stage_kernel_cl<MS, TH, TW, RF, RB, NT, FAST, F, MINB>;
         int rc = prepare(kern, dev, attr_set, mu);
         if (rc) return rc;
+        set_groups((a.nk + F - 1) / F);
         CUDA_TRY(launch_pdl_cluster(kern, grid, NT, C::smem_bytes(a.tab_stride), cl, s, b));
         g_launches.fetch_add(1);
         return TNRD_OK;
@@ -1681,6 +1690,7 @@ static StageArgs stage_args(const tnrd_model* md, int t, uint32_t flags) {
     a.stage = t;
     a.status = nullptr;
     a.force_out = nullptr;
+    a.cluster = 1; a.cl_gper = 0; a.cl_gextra = 0; a.cl_tiles_x = 1;
     return a;
 }
 

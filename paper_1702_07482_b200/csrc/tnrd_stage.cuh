@@ -110,6 +110,9 @@ struct StageArgs {
     int stage;
     uint32_t* status;    // [0] first non-finite stage (atomicMin), [1] f flags (atomicAnd ~bit)
     float* force_out;    // optional second output: the force (tnrd_stage_force), same layout as u_out
+    // stage_kernel_cl*: CTAs per cluster (= gridDim.x), groups per rank and
+    // ranks with one more, tiles per image row (blockIdx.y = tile_y * cl_tiles_x + tile_x)
+    int cluster, cl_gper, cl_gextra, cl_tiles_x;
 };
 
 __device__ __forceinline__ float ex2f(float x) {
@@ -756,21 +759,63 @@ __device__ __forceinline__ void forward_block_p2(const StageArgs& p, const float
     }
 }
 
+// Mirrored phi halo without a fix-up pass (EDGE variants of the backward
+// filters).  The reference pads phi itself (diffusion.py:180): a phi value
+// outside the image is the in-image value at the mirrored position.  When an
+// image edge coincides with the tile edge (always on the left / top; on the
+// right / bottom when the tile is full) the mirrored positions of a thread's
+// RB+2R x 4+2R window lie in the window itself: a window row outside the
+// image is READ at its mirrored row (edge_row: region row 2R-1-y above the
+// image, 2(TH+R)-1-y below; compile-time row offsets when RB >= R), and after
+// a row is loaded its out-of-image columns take the registers of the
+// mirrored columns (edge_cols: col c < R <- col 2R-1-c on the left, col
+// 4+R+c <- col 4+R-1-c on the right; only the first / last output block of a
+// row sees them).  `ef` bits (per thread): 1 left, 2 right, 4 top, 8 bottom
+// edge inside this thread's window.  The out-of-image phi cells keep what the
+// forward stored there; nobody reads them.  Same values in the same FMA
+// order as after the fix_phi pass, so the same bits (tools/ab_outputs.py).
+// Ragged right / bottom tiles use fix_phi and the plain variants.
+template <class C, int RB>
+__device__ __forceinline__ int edge_row(int rr, int oy0, uint32_t ef) {
+    constexpr int R = C::R;
+    constexpr int TH = C::OBY * RB;
+    if constexpr (RB >= R) {
+        // out-of-image rows only in the first / last thread row: static remap
+        if (rr < R) return oy0 + ((ef & 4u) ? 2 * R - 1 - rr : rr);
+        if (rr >= RB + R) return oy0 + ((ef & 8u) ? 2 * (RB + R) - 1 - rr : rr);
+        return oy0 + rr;
+    } else {
+        int row = oy0 + rr;
+        if ((ef & 4u) && row < R) row = 2 * R - 1 - row;
+        if ((ef & 8u) && row >= TH + R) row = 2 * (TH + R) - 1 - row;
+        return row;
+    }
+}
+template <int R, int N>
+__device__ __forceinline__ void edge_cols(float (&v)[N], uint32_t ef) {
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+        v[c] = (ef & 1u) ? v[2 * R - 1 - c] : v[c];
+        v[4 + R + c] = (ef & 2u) ? v[4 + R - 1 - c] : v[4 + R + c];
+    }
+}
+
 // backward_filter with FFMA2 row pairs: force2[q] = rows (2q, 2q+1)
-template <class C, int MS, int RB>
+template <class C, int MS, int RB, bool EDGE = false>
 __device__ __forceinline__ void backward_filter_p2(const float* ph, const float* kq, int ox0, int oy0,
-                                                   f2_t (&force2)[RB / 2][4]) {
+                                                   f2_t (&force2)[RB / 2][4], uint32_t ef = 0u) {
     constexpr int R = C::R;
     static_assert(RB % 2 == 0, "row pairs");
 #pragma unroll
     for (int rr = 0; rr < RB + 2 * R; ++rr) {
         float v[4 * C::NV];
-        const float* src = ph + (oy0 + rr) * C::PW + ox0;
+        const float* src = ph + (EDGE ? edge_row<C, RB>(rr, oy0, ef) : oy0 + rr) * C::PW + ox0;
 #pragma unroll
         for (int q = 0; q < C::NV; ++q) {
             const float4 t = lds128(src + 4 * q);
             v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
         }
+        if constexpr (EDGE) edge_cols<R>(v, ef);
 #pragma unroll
         for (int q = 0; q < RB / 2; ++q) {
             const int a0 = rr - 2 * q;   // tap row of k for output row 2q
@@ -892,19 +937,20 @@ __device__ __forceinline__ void fix_phi(const StageArgs& p, float* sPhi, int Y0,
 
 // backward of one filter: force += corr(phi_i, k_i) over this thread's
 // RB x 4 output block (K: register taps or a parameter-space pointer)
-template <class C, int MS, int RB, class K>
+template <class C, int MS, int RB, bool EDGE = false, class K>
 __device__ __forceinline__ void backward_filter(const float* ph, const K& k, int ox0, int oy0,
-                                                float (&force)[RB][4]) {
+                                                float (&force)[RB][4], uint32_t ef = 0u) {
     constexpr int R = C::R;
 #pragma unroll
     for (int rr = 0; rr < RB + 2 * R; ++rr) {
         float v[4 * C::NV];
-        const float* src = ph + (oy0 + rr) * C::PW + ox0;
+        const float* src = ph + (EDGE ? edge_row<C, RB>(rr, oy0, ef) : oy0 + rr) * C::PW + ox0;
 #pragma unroll
         for (int q = 0; q < C::NV; ++q) {
             const float4 t = lds128(src + 4 * q);
             v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
         }
+        if constexpr (EDGE) edge_cols<R>(v, ef);
 #pragma unroll
         for (int a = 0; a < MS; ++a) {
             const int ro = rr - a;
@@ -921,14 +967,14 @@ __device__ __forceinline__ void backward_filter(const float* ph, const K& k, int
 }
 
 // backward: force += corr(phi_i, k_i) for this thread's filters of the group
-template <class C, int MS, int RB, int F>
+template <class C, int MS, int RB, int F, bool EDGE = false>
 __device__ __forceinline__ void backward_group(const float* sPhi, const float* tapg, int split,
-                                               int ox0, int oy0, float (&force)[RB][4]) {
+                                               int ox0, int oy0, float (&force)[RB][4], uint32_t ef = 0u) {
 #pragma unroll 1
     for (int fi = split; fi < F; fi += C::NSPLIT) {
         float k[C::KK];
         load_taps<C>(tapg + fi * C::KP, k);
-        backward_filter<C, MS, RB>(sPhi + fi * C::SPHI, k, ox0, oy0, force);
+        backward_filter<C, MS, RB, EDGE>(sPhi + fi * C::SPHI, k, ox0, oy0, force, ef);
     }
 }
 
@@ -962,18 +1008,18 @@ struct ForceAcc {
 // written with pointer increments and a __syncwarp, the form in which ptxas
 // keeps the taps in uniform registers (a plain indexed unroll-1 loop loads
 // them into per-thread registers with LDC)
-template <class C, int MS, int RB, int F, int TM>
+template <class C, int MS, int RB, int F, int TM, bool EDGE = false>
 __device__ __forceinline__ void backward_group_pt(const float* sPhi, const float* kg, int ox0, int oy0,
-                                                  ForceAcc<MS, RB, (TM == 1 || TM == 2)>& acc) {
+                                                  ForceAcc<MS, RB, (TM == 1 || TM == 2)>& acc, uint32_t ef = 0u) {
     static_assert(C::NSPLIT == 1, "parameter-space taps need one thread per output block");
     using TL = TapLayout<MS, C::KP, F, TM>;
     const float* k = kg + TL::bwd0;
     const float* ph = sPhi;
 #pragma unroll 1
     for (int fi = 0; fi < F; ++fi, k += TL::per_filter, ph += C::SPHI) {
-        if constexpr (TM == 1 || TM == 2) backward_filter_p2<C, MS, RB>(ph, k, ox0, oy0, acc.f2);
-        else if constexpr (TM == 3) backward_filter<C, MS, RB>(ph, FpTap<MS>{k}, ox0, oy0, acc.f1);
-        else backward_filter<C, MS, RB>(ph, k, ox0, oy0, acc.f1);
+        if constexpr (TM == 1 || TM == 2) backward_filter_p2<C, MS, RB, EDGE>(ph, k, ox0, oy0, acc.f2, ef);
+        else if constexpr (TM == 3) backward_filter<C, MS, RB, EDGE>(ph, FpTap<MS>{k}, ox0, oy0, acc.f1, ef);
+        else backward_filter<C, MS, RB, EDGE>(ph, k, ox0, oy0, acc.f1, ef);
         __syncwarp();
     }
 }
@@ -1133,6 +1179,12 @@ constexpr int kMaxCluster = 8;   // portable cluster size limit
 // ---- tile kernel: one CTA = one output tile, all filter groups -------------
 // PT: taps read from the parameter space (`kp` = this stage's TapBlock)
 // instead of being staged in shared memory and held in registers
+// mirrored phi halo inside the backward's window instead of the fix_phi pass
+// (tile and cluster kernels; 0 = always fix_phi, for A/B runs)
+#ifndef TNRD_EDGE_BACKWARD
+#define TNRD_EDGE_BACKWARD 1
+#endif
+
 #ifdef TNRD_PHASE_TRACE
 // per-phase CTA clock totals of the tile kernel (tools/phase_trace.py):
 // 0 staging, 1 forward + RBF, 2 phi fix-up + table fetch, 3 backward (to the
@@ -1164,12 +1216,21 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
 
     const int tid = threadIdx.x;
     const int img = blockIdx.z;
-    const int Y0 = blockIdx.y * TH;
-    const int clr = CLU ? (int)cluster_ctarank() : 0;    // this CTA's share of the groups
-    const int cln = CLU ? (int)cluster_nctarank() : 1;
-    const int X0 = (CLU ? (int)blockIdx.x / cln : (int)blockIdx.x) * TW;
-    const int gbeg = CLU ? (p.ngroups * clr) / cln : 0;
-    const int gend = CLU ? (p.ngroups * (clr + 1)) / cln : p.ngroups;
+    // Cluster launches: grid (cluster, tiles, batch), the cluster along x, so
+    // the rank is blockIdx.x and this CTA's group range -- the rank-th of
+    // `cluster` contiguous ranges, the first cl_gextra one group longer --
+    // needs no division.  (With %cluster_ctarank, or a division by the
+    // cluster size, ptxas computed the group index outside the uniform
+    // datapath in some instantiations -- m = 9, m = 3 -- and the taps fell
+    // back to per-thread LDC; SASS checked.)
+    const int cln = CLU ? p.cluster : 1;
+    const int clr = CLU ? (int)blockIdx.x : 0;
+    const int tile_y = CLU ? (int)blockIdx.y / p.cl_tiles_x : (int)blockIdx.y;
+    const int tile_x = CLU ? (int)blockIdx.y - tile_y * p.cl_tiles_x : (int)blockIdx.x;
+    const int Y0 = tile_y * TH;
+    const int X0 = tile_x * TW;
+    const int gbeg = CLU ? clr * p.cl_gper + min(clr, p.cl_gextra) : 0;
+    const int gend = CLU ? gbeg + p.cl_gper + (clr < p.cl_gextra ? 1 : 0) : p.ngroups;
     const float* __restrict__ uin = p.u_in + (int64_t)img * p.img_stride;
     const float* __restrict__ fin = p.f + (int64_t)img * p.img_stride;
     float* __restrict__ uout = p.u_out + (int64_t)img * p.img_stride;
@@ -1198,6 +1259,21 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
     const int split = PT ? 0 : tid / (C::OBX * C::OBY);  // which filters of a group
     const int obx = tid % C::OBX, oby = (tid / C::OBX) % C::OBY;
     const int ox0 = obx * 4, oy0 = oby * RB;
+    // image edges in this tile's phi region: when they coincide with the
+    // tile's edges the backward mirrors phi inside its own window (EDGE
+    // variants: edge_row / edge_cols, no fix-up pass); ragged right / bottom
+    // tiles run fix_phi
+    uint32_t ef = 0u;
+    bool edge_static = false;
+    if constexpr (TNRD_EDGE_BACKWARD) {
+        const bool fix_l = X0 - R < 0, fix_r = X0 + TW + R > p.W;
+        const bool fix_t = !top_halo && Y0 - R < 0, fix_b = !bot_halo && Y0 + TH + R > p.H;
+        edge_static = (fix_l || fix_r || fix_t || fix_b) && (!fix_r || p.W - X0 == TW) &&
+                      (!fix_b || p.H - Y0 == TH);
+        if (edge_static)
+            ef = (fix_l && obx == 0 ? 1u : 0u) | (fix_r && obx == C::OBX - 1 ? 2u : 0u) |
+                 (fix_t && oy0 < R ? 4u : 0u) | (fix_b && oy0 + RB + R > TH ? 8u : 0u);
+    }
     constexpr int GS = TapLayout<MS, C::KP, F, TM>::group;   // PT tap floats per filter group
     float force[RB][4];
     ForceAcc<MS, RB, (TM == 1 || TM == 2)> facc;   // PT: FFMA2 row pairs (TM 1, 2) or scalars
@@ -1224,10 +1300,16 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
         // PT: the table is free -- fetch the next group's under fix-up + backward
         if constexpr (PT)
             if (tid == 0 && g + 1 < gend) tbar_fetch(sTab, p.tab3 + (size_t)(g + 1) * tabsz, tabsz, &tbar);
-        fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
-        TNRD_PHASE_MARK(2)
-        if constexpr (PT) backward_group_pt<C, MS, RB, F, TM>(sPhi, tapg, ox0, oy0, facc);
-        else backward_group<C, MS, RB, F>(sPhi, tapg, split, ox0, oy0, force);
+        if (edge_static) {
+            TNRD_PHASE_MARK(2)
+            if constexpr (PT) backward_group_pt<C, MS, RB, F, TM, true>(sPhi, tapg, ox0, oy0, facc, ef);
+            else backward_group<C, MS, RB, F, true>(sPhi, tapg, split, ox0, oy0, force, ef);
+        } else {
+            fix_phi<C, F, NT, TH, TW>(p, sPhi, Y0, X0, top_halo, bot_halo, tid);
+            TNRD_PHASE_MARK(2)
+            if constexpr (PT) backward_group_pt<C, MS, RB, F, TM>(sPhi, tapg, ox0, oy0, facc);
+            else backward_group<C, MS, RB, F>(sPhi, tapg, split, ox0, oy0, force);
+        }
     }
     if constexpr (PT) {
 #pragma unroll

@@ -121,3 +121,31 @@ def test_c_example_compiles_against_the_header():
                             "-L", os.path.join(repo, "paper_1702_07482_b200"), "-ltnrd",
                             "-lm", "-o", exe], capture_output=True, text=True)
         assert r.returncode == 0, r.stderr
+
+
+def test_parameter_space_kernels_keep_the_uniform_datapath():
+    """The parameter-space-taps kernels (tile, cluster and split variants) must
+    read their taps through the uniform datapath -- FFMA / FFMA2 with a
+    uniform-register (UR) operand fed by LDCU.  ptxas silently falls back to
+    per-thread LDC loads when it cannot prove the filter-group index uniform
+    (seen on B200 builds: a cluster rank taken from %cluster_ctarank, an
+    integer division in the group range, a per-thread copy loop in the group
+    loop), which costs ~15% (C5).  Checked on the shipped library's SASS."""
+    import re
+    import shutil
+    import subprocess
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    LIB = _lib.LIB_PATH
+    if not os.path.exists(cuobjdump) or not os.path.exists(LIB):
+        pytest.skip("cuobjdump or libtnrd.so not available")
+    sass = subprocess.run([cuobjdump, "-sass", LIB], capture_output=True, text=True, check=True).stdout
+    seen = 0
+    for part in re.split(r"\n\s*Function : ", sass)[1:]:
+        name = part.split("\n", 1)[0].strip()
+        if not re.search(r"stage_kernel_(cl_pt|pt|split_pt)I", name):
+            continue
+        seen += 1
+        fma = len(re.findall(r"\bFFMA2?\b", part))
+        fma_ur = len(re.findall(r"\bFFMA2?\b[^;]*\bUR\d+", part))
+        assert fma > 300 and fma_ur >= 0.35 * fma, (name[:80], fma, fma_ur)   # broken builds: < 2%
+    assert seen >= 12, seen   # m = 3, 5, 7, 9 x tile / cluster / split

@@ -49,6 +49,29 @@ def test_edge_shapes_both_tiles(tiles, oracle, H, W, m):
     assert parity_stats(u, ref)["rel"] <= 1e-4
 
 
+@pytest.mark.parametrize("mode", [_lib.KERNEL_SMALL_TILES, _lib.KERNEL_LARGE_TILES,
+                                  _lib.KERNEL_CLUSTER_LARGE, _lib.KERNEL_CLUSTER_SMALL],
+                         ids=["small", "large", "cluster_large", "cluster_small"])
+@pytest.mark.parametrize("H,W,m", [(64, 64, 7), (128, 192, 7), (64, 128, 3), (192, 64, 5), (128, 128, 9),
+                                   (64, 67, 7), (66, 64, 7), (32, 96, 5)])
+def test_tile_aligned_edges_mirror_in_the_backward_window(cuda, oracle, mode, H, W, m):
+    """Image edges that coincide with tile edges: the tile / cluster kernels
+    mirror phi inside the backward's own window (no fix-up pass; reference
+    pads phi itself, diffusion.py:180).  Single-tile images (all four edges
+    in one tile), multi-tile ones, and images 2-3 pixels larger than a tile
+    (the out-of-image band is narrower than r: fix-up pass) against the
+    oracle."""
+    _lib.set_stage_kernel(mode)
+    try:
+        model = synth.make_model(m, 6, 2, 63, seed=H + W + m)
+        f = np.random.default_rng(H * W).uniform(0, 300, (H, W)).astype(np.float32)
+        u, _ = tn.run_diffusion(f, model)
+    finally:
+        _lib.set_stage_kernel(_lib.KERNEL_AUTO)
+    ref = oracle.run_diffusion(f.astype(np.float64), model)
+    assert parity_stats(u, ref)["rel"] <= 1e-4
+
+
 def test_c2_full_both_tiles(tiles, oracle):
     cfg = synth.CONFIGS["c2"]
     clean, f = synth.noisy_image(cfg, 0)

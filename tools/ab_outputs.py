@@ -20,8 +20,13 @@ cases = {
     "m3": (synth.make_model(3, 10, 2, 63, seed=4), rng.uniform(1, 255, (8, 300, 260)).astype(np.float32)),
     "m5": (synth.make_model(5, 13, 2, 63, seed=5), rng.uniform(1, 255, (8, 260, 300)).astype(np.float32)),
     "c5x2": (synth.config_model(synth.CONFIGS["c5"]), synth.noisy_batch(synth.CONFIGS["c5"], range(2))),
+    # tile-aligned shapes: every image edge is a tile edge (EDGE backward variants)
+    "m3a": (synth.make_model(3, 10, 2, 63, seed=4), rng.uniform(1, 255, (3, 128, 192)).astype(np.float32)),
+    "m5a": (synth.make_model(5, 13, 2, 63, seed=5), rng.uniform(1, 255, (2, 64, 64)).astype(np.float32)),
+    "m9a": (synth.make_model(9, 6, 2, 63, seed=6), rng.uniform(1, 255, (192, 64)).astype(np.float32)),
 }
-for mode in (_lib.KERNEL_AUTO, _lib.KERNEL_LARGE_TILES, _lib.KERNEL_SPLIT_LARGE):
+for mode in (_lib.KERNEL_AUTO, _lib.KERNEL_SMALL_TILES, _lib.KERNEL_LARGE_TILES, _lib.KERNEL_SPLIT_LARGE,
+             _lib.KERNEL_CLUSTER_LARGE, _lib.KERNEL_CLUSTER_SMALL):
     _lib.set_stage_kernel(mode)
     for k, (model, f) in cases.items():
         dm = tn.device_model_for(model)
