@@ -86,6 +86,17 @@ extern "C" uint32_t tnrd_build_features(void) {
 #endif
 }
 extern "C" void tnrd_launch_count_reset(void) { g_launches.store(0); }
+#ifdef TNRD_BOUNDS
+// debug bounds mode (tnrd_stage.cuh TNRD_ASSERT): violations so far --
+// out4 = {count, kind, value, limit of the first}; clears the counters
+extern "C" __attribute__((visibility("default"))) int tnrd_bounds_failures(unsigned int* out4) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpyFromSymbol(out4, g_bounds_fail, 4 * sizeof(unsigned int)));
+    unsigned int z[4] = {0, 0, 0, 0};
+    CUDA_TRY(cudaMemcpyToSymbol(g_bounds_fail, z, sizeof(z)));
+    return TNRD_OK;
+}
+#endif
 #ifdef TNRD_PHASE_TRACE
 // tools/phase_trace.py: read (and clear) the tile kernel's per-phase clocks
 extern "C" __attribute__((visibility("default"))) int tnrd_phase_trace(unsigned long long* out8) {

@@ -115,6 +115,26 @@ struct StageArgs {
     int cluster, cl_gper, cl_gextra, cl_tiles_x;
 };
 
+// Debug bounds mode (-DTNRD_BOUNDS, tools/bounds_run.sh): every shared-memory
+// index computed at run time -- forward / backward block extents, RBF table
+// lookups, the phi fix-up, split / cluster partial stores -- and the image
+// coordinates of the global accesses are checked against their buffer;
+// violations are counted (first one kept) in g_bounds_fail and read back with
+// tnrd_bounds_failures().  compute-sanitizer is closed on the GPU pool, so
+// this build is the memory-safety evidence: the GPU test suite must finish
+// with zero violations (profiles/r02_bounds).
+#ifdef TNRD_BOUNDS
+__device__ unsigned int g_bounds_fail[4];   // count, kind, value, limit of the first
+__device__ __forceinline__ void bounds_fail(unsigned kind, unsigned v, unsigned lim) {
+    if (atomicAdd(&g_bounds_fail[0], 1u) == 0u) {
+        g_bounds_fail[1] = kind; g_bounds_fail[2] = v; g_bounds_fail[3] = lim;
+    }
+}
+#define TNRD_ASSERT(cond, kind, v, lim) do { if (!(cond)) bounds_fail(kind, (unsigned)(v), (unsigned)(lim)); } while (0)
+#else
+#define TNRD_ASSERT(cond, kind, v, lim) do { } while (0)
+#endif
+
 __device__ __forceinline__ float ex2f(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -251,6 +271,7 @@ __device__ __forceinline__ float rbf_poly_s(float z, uint32_t tb, const StageArg
     const float x = t - (r - 12582912.0f);
     const uint32_t b = static_cast<uint32_t>(__float_as_int(r));
     const uint32_t a = ((b >> 3) << 7) + (b << 4) + tb;
+    TNRD_ASSERT((a - (tb - p.tab_bias)) + 144u <= 4u * (uint32_t)p.tab_stride && !(a & 15u), 3, a - (tb - p.tab_bias), 4 * p.tab_stride);
     float4 lo, hi;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%8];\n\t"
                  "ld.shared.v4.f32 {%4, %5, %6, %7}, [%8+128];"
@@ -272,6 +293,7 @@ __device__ __forceinline__ float rbf_cubic_s(float z, uint32_t tb3, const StageA
     const float r = t + 12582912.0f;
     const float x = t - (r - 12582912.0f);
     const uint32_t a = (static_cast<uint32_t>(__float_as_int(r)) << 4) + tb3;
+    TNRD_ASSERT((a - (tb3 - p.tab3_bias)) + 16u <= 4u * (uint32_t)p.tab3_stride && !(a & 15u), 3, a - (tb3 - p.tab3_bias), 4 * p.tab3_stride);
     float4 c;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(c.x), "=f"(c.y), "=f"(c.z), "=f"(c.w)
@@ -345,6 +367,7 @@ __device__ __forceinline__ void stage_u_tile(const StageArgs& p, float* sU, cons
                 const int X = mirror_clamp(X0 - 2 * R + ux, p.W);
                 if (Y < 0) Y = top_halo ? max(Y, -2 * R) : mirror_clamp(Y, p.H);
                 else if (Y >= p.H) Y = bot_halo ? min(Y, p.H - 1 + 2 * R) : mirror_clamp(Y, p.H);
+                TNRD_ASSERT(X >= 0 && X < p.W && Y >= (top_halo ? -2 * R : 0) && Y < p.H + (bot_halo ? 2 * R : 0), 5, Y, p.H);
                 v[j] = COHERENT ? __ldcg(uin + (int64_t)Y * p.ld + X) : __ldg(uin + (int64_t)Y * p.ld + X);
             }
         }
@@ -424,6 +447,8 @@ __device__ __forceinline__ void forward_block(const StageArgs& p, const float* s
     const int by = blk / C::NBX;
     const int bx = blk - by * C::NBX;
     const int x0 = bx * 4, y0 = by * RF;
+    TNRD_ASSERT(blk >= 0 && blk < C::NBLK && y0 + RF + 2 * R <= C::UR && x0 + 4 * C::NV <= C::US &&
+                y0 + RF <= C::PH && x0 + 4 <= C::PW, 1, blk, C::NBLK);
     float* dst = phif + y0 * C::PW + x0;
     float acc[RF][4];
 #pragma unroll
@@ -587,6 +612,8 @@ __device__ __forceinline__ void forward_block_fp(const StageArgs& p, const float
     const int by = blk / C::NBX;
     const int bx = blk - by * C::NBX;
     const int x0 = bx * 4, y0 = by * RF;
+    TNRD_ASSERT(blk >= 0 && blk < C::NBLK && y0 + RF + 2 * R <= C::UR && x0 + 4 * C::NV <= C::US &&
+                y0 + RF <= C::PH && x0 + 4 <= C::PW, 1, blk, C::NBLK);
     float* d0 = phi0 + y0 * C::PW + x0;
     float* d1 = phi1 + y0 * C::PW + x0;
     f2_t acc2[RF][4];
@@ -674,6 +701,8 @@ __device__ __forceinline__ void forward_block_p2(const StageArgs& p, const float
     const int by = blk / C::NBX;
     const int bx = blk - by * C::NBX;
     const int x0 = bx * 4, y0 = by * RF;
+    TNRD_ASSERT(blk >= 0 && blk < C::NBLK && y0 + RF + 2 * R <= C::UR && x0 + 4 * C::NV <= C::US &&
+                y0 + RF <= C::PH && x0 + 4 <= C::PW, 1, blk, C::NBLK);
     f2_t acc2[NP][4];
     float accs[4];
 #pragma unroll
@@ -809,7 +838,9 @@ __device__ __forceinline__ void backward_filter_p2(const float* ph, const float*
 #pragma unroll
     for (int rr = 0; rr < RB + 2 * R; ++rr) {
         float v[4 * C::NV];
-        const float* src = ph + (EDGE ? edge_row<C, RB>(rr, oy0, ef) : oy0 + rr) * C::PW + ox0;
+        const int row_ = EDGE ? edge_row<C, RB>(rr, oy0, ef) : oy0 + rr;
+        TNRD_ASSERT(row_ >= 0 && row_ < C::PH && ox0 >= 0 && ox0 + 4 * C::NV <= C::PW, 2, row_, C::PH);
+        const float* src = ph + row_ * C::PW + ox0;
 #pragma unroll
         for (int q = 0; q < C::NV; ++q) {
             const float4 t = lds128(src + 4 * q);
@@ -929,6 +960,8 @@ __device__ __forceinline__ void fix_phi(const StageArgs& p, float* sPhi, int Y0,
         else if (!bot_halo && Y >= p.H && Y < p.H + R) sy = 2 * p.H - 1 - Y;
         if (sy != Y || sx != X) {
             const int spy = sy - (Y0 - R), spx = sx - (X0 - R);
+            TNRD_ASSERT(j < F && py >= 0 && py < C::PH && px >= 0 && px < C::PW && spy >= 0 && spy < C::PH &&
+                        spx >= 0 && spx < C::PW, 4, spy * C::PW + spx, C::SPHI);
             sPhi[j * C::SPHI + py * C::PW + px] = sPhi[j * C::SPHI + spy * C::PW + spx];
         }
     }
@@ -944,7 +977,9 @@ __device__ __forceinline__ void backward_filter(const float* ph, const K& k, int
 #pragma unroll
     for (int rr = 0; rr < RB + 2 * R; ++rr) {
         float v[4 * C::NV];
-        const float* src = ph + (EDGE ? edge_row<C, RB>(rr, oy0, ef) : oy0 + rr) * C::PW + ox0;
+        const int row_ = EDGE ? edge_row<C, RB>(rr, oy0, ef) : oy0 + rr;
+        TNRD_ASSERT(row_ >= 0 && row_ < C::PH && ox0 >= 0 && ox0 + 4 * C::NV <= C::PW, 2, row_, C::PH);
+        const float* src = ph + row_ * C::PW + ox0;
 #pragma unroll
         for (int q = 0; q < C::NV; ++q) {
             const float4 t = lds128(src + 4 * q);
@@ -1300,6 +1335,11 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
         // PT: the table is free -- fetch the next group's under fix-up + backward
         if constexpr (PT)
             if (tid == 0 && g + 1 < gend) tbar_fetch(sTab, p.tab3 + (size_t)(g + 1) * tabsz, tabsz, &tbar);
+#ifdef TNRD_PROBE_NO_BACKWARD
+        // perf probe only (wrong results): the stage without its adjoint
+        // convolution = the ceiling of any tensor-core offload of the backward
+        if (p.H > 0) continue;
+#endif
         if (edge_static) {
             TNRD_PHASE_MARK(2)
             if constexpr (PT) backward_group_pt<C, MS, RB, F, TM, true>(sPhi, tapg, ox0, oy0, facc, ef);
@@ -1332,9 +1372,11 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
         float* sPart = sPhi + (C::NSPLIT - 1) * TPX;
         if (full) {
 #pragma unroll
-            for (int r = 0; r < RB; ++r)
+            for (int r = 0; r < RB; ++r) {
+                TNRD_ASSERT((oy0 + r) * TW + ox0 + 4 <= TPX, 8, (oy0 + r) * TW + ox0, TPX);
                 *reinterpret_cast<float4*>(sPart + (oy0 + r) * TW + ox0) =
                     make_float4(force[r][0], force[r][1], force[r][2], force[r][3]);
+            }
         }
         cluster_sync_all();   // every CTA's partial is visible cluster-wide
         constexpr int QUADS = TPX / 4;
@@ -1345,6 +1387,7 @@ __device__ __forceinline__ void stage_tile_body(const StageArgs& p, const float*
         uint32_t fbits = 0;
         for (int q = clr * qs + tid; q < qend; q += NT) {
             const int y = (4 * q) / TW, x = (4 * q) % TW;
+            TNRD_ASSERT(q >= 0 && q < QUADS && y < TH && (y + 2 * R) * C::US + x + 3 + 2 * R < C::SU, 8, q, QUADS);
             float4 v[kMaxCluster];
 #pragma unroll
             for (int r = 0; r < kMaxCluster; ++r)
@@ -1676,9 +1719,11 @@ __device__ __forceinline__ void stage_split_body_pt(const StageArgs& p, const Sp
             facc.zero();
             backward_group_pt<C, MS, RB, F, TM>(sPhi, tapg, ox0, oy0, facc);
 #pragma unroll
-            for (int r = 0; r < RB; ++r)
+            for (int r = 0; r < RB; ++r) {
+                TNRD_ASSERT(tile < ws.tiles && g < ng && oy0 * TW + ox0 + r * TW + 4 <= TPX, 7, tile, ws.tiles);
                 __stcg(reinterpret_cast<float4*>(dst + (size_t)g * TPX + r * TW),
                        make_float4(facc.get(r, 0), facc.get(r, 1), facc.get(r, 2), facc.get(r, 3)));
+            }
         }
     }
     fills += nunits;

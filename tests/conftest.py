@@ -18,6 +18,31 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running parity case")
 
 
+def pytest_sessionfinish(session, exitstatus):
+    """Debug bounds build (-DTNRD_BOUNDS, tools/bounds_run.sh): after the
+    suite, the library's violation counters must be zero."""
+    try:
+        from paper_1702_07482_b200 import _lib
+        L = _lib._lib
+        if L is None or not hasattr(L, "tnrd_bounds_failures"):
+            return
+        import ctypes
+        out = (ctypes.c_uint * 4)()
+        L.tnrd_bounds_failures.restype = ctypes.c_int
+        rc = L.tnrd_bounds_failures(out)
+        line = (f"TNRD_BOUNDS: rc {rc}, {out[0]} violations"
+                + (f" (first: kind {out[1]}, value {out[2]}, limit {out[3]})" if out[0] else ""))
+        print("\n" + line)
+        path = os.environ.get("TNRD_BOUNDS_REPORT")
+        if path:
+            with open(path, "a") as fh:
+                fh.write(line + "\n")
+        if rc != 0 or out[0]:
+            session.exitstatus = 1
+    except Exception as e:  # never mask the suite's own result
+        print(f"\nTNRD_BOUNDS: report failed: {e}")
+
+
 def golden_names(full_only=False):
     out = []
     for p in sorted(glob.glob(os.path.join(GOLDEN, "*.npz"))):
