@@ -127,10 +127,17 @@ int tnrd_model_rbf_fit_cubic(const tnrd_model* model, double* max_abs_err,
  * CTAs of a thread-block cluster split a tile's filter groups, keep their
  * partial forces in shared memory and sum them in rank order through
  * distributed shared memory, each CTA finishing its share of the tile's
- * pixels (diffusion_step, diffusion.py:184-194, as one operator).  Auto
- * runs the split kernel on grids below 3 waves of large tiles; it keeps a
- * partial-force workspace per stream inside the model (allocated on first
- * use, outside stream capture). */
+ * pixels (diffusion_step, diffusion.py:184-194, as one operator), 12 =
+ * tensor-core adjoint (two launches per stage: a CUDA-core kernel writes
+ * phi = RBF(conv(u, k)) once per pixel, a tcgen05 kernel runs the adjoint
+ * filter bank as a 3xTF32 GEMM with the shifted sum and the reaction in its
+ * epilogue; m = 5, 7; other models and strip launches silently use the
+ * CUDA-core kernels; opt-in: parity-green but measured slower than the fused
+ * kernel on B200; keeps a phi workspace per stream inside
+ * the model).  Auto runs the tile kernel from 6 waves of large tiles and the
+ * cluster kernel below (one launch per stage either way); the split kernel
+ * (modes 6 / 7) keeps a partial-force workspace per stream inside the model
+ * (allocated on first use, outside stream capture). */
 int tnrd_set_stage_kernel(int mode);
 /* CTAs per cluster of the cluster kernel: 0 = chosen from the grid size
  * (the largest cluster <= 8 whose CTAs fit one wave), 2..8 = forced.  The

@@ -156,11 +156,13 @@ KERNEL_TC_PHASED = 5
 KERNEL_SPLIT_LARGE, KERNEL_SPLIT_SMALL = 6, 7
 KERNEL_ZFIELD = 8
 KERNEL_CLUSTER_LARGE, KERNEL_CLUSTER_SMALL = 10, 11
+KERNEL_TC_ADJOINT = 12
 
 
 def set_stage_kernel(mode: int) -> None:
-    """0 auto, 1 CUDA-core, 2 tcgen05 forward GEMM, 3/4 CUDA-core with
-    small/large tiles forced."""
+    """0 auto, 1 CUDA-core, 2 tcgen05 forward GEMM, 3/4 CUDA-core tile
+    kernel with small/large tiles forced, 6/7 split kernel, 10/11 cluster
+    kernel, 12 tensor-core adjoint (include/tnrd.h)."""
     check(load().tnrd_set_stage_kernel(int(mode)))
 
 

@@ -23,6 +23,7 @@
 
 #include "../../include/tnrd.h"
 #include "tnrd_stage.cuh"
+#include "tnrd_stage_adj.cuh"
 #include "tnrd_speckle.cuh"
 #include "tnrd_train.cuh"
 // The tensor-core and dataflow stage kernels measured slower than the
@@ -159,6 +160,12 @@ struct tnrd_model {
     mutable std::map<cudaStream_t, SplitBuf> fws;
     // z-field planes (tnrd_stage_zf.cuh), one per stream
     mutable std::map<cudaStream_t, SplitBuf> zws;
+    // tensor-core adjoint (tnrd_stage_adj.cuh, mode 12): the GEMM's B operand
+    // (per stage [ks][2 prec][2 kc][NB][4], built on first use) and the phi
+    // workspaces, one per stream
+    mutable float* d_aop = nullptr;
+    mutable size_t aop_stage = 0;
+    mutable std::map<cudaStream_t, SplitBuf> aws;
     // batch fork (tnrd_despeckle): per caller stream, a second stream and
     // the fork / join events (DESIGN.md §7b item 5)
     struct ForkRes { cudaStream_t s2 = nullptr; cudaEvent_t fork = nullptr, join = nullptr; };
@@ -186,7 +193,7 @@ extern "C" int tnrd_set_param_taps(int on) {
 }
 
 extern "C" int tnrd_set_stage_kernel(int mode) {
-    if (mode < 0 || mode > 11) return fail(TNRD_EINVAL, "stage kernel mode must be in 0..11");
+    if (mode < 0 || mode > 12) return fail(TNRD_EINVAL, "stage kernel mode must be in 0..12");
     g_kernel_mode.store(mode);
     return TNRD_OK;
 }
@@ -509,6 +516,8 @@ extern "C" int tnrd_model_destroy(tnrd_model* md) {
         for (void* q : md->retired) cudaFree(q);
         for (auto& kv : md->ws) cudaFree(kv.second.ptr);
         for (auto& kv : md->zws) cudaFree(kv.second.ptr);
+        for (auto& kv : md->aws) cudaFree(kv.second.ptr);
+        cudaFree(md->d_aop);
         for (auto& kv : md->fws) cudaFree(kv.second.ptr);
         for (auto& kv : md->forks) {
             cudaStreamSynchronize(kv.second.s2);
@@ -1705,6 +1714,141 @@ static StageArgs stage_args(const tnrd_model* md, int t, uint32_t flags) {
     return a;
 }
 
+
+// ---- tensor-core adjoint stage (tnrd_stage_adj.cuh, mode 12) ---------------
+// B operand of the adjoint GEMM psi = Phi K^T for every stage: K-major
+// [ks][prec][kc][n][e] = piece_prec(k_i[n]), i = 8 ks + 4 kc + e, n = the tap
+// index a m + b of the reference kernel k_i (zero for n >= m^2, i >= nk);
+// prec 0 = tf32 rna(k), 1 = rna(k - hi).
+static int adj_operand(const tnrd_model* md, int nb, int kc) {
+    std::lock_guard<std::mutex> lk(md->ws_mu);
+    if (md->d_aop) return TNRD_OK;
+    const int ks = kc / 2, mm = md->m * md->m;
+    const size_t per_stage = (size_t)ks * 2 * 2 * nb * 4;
+    std::vector<float> h((size_t)md->T * per_stage, 0.0f);
+    for (int t = 0; t < md->T; ++t)
+        for (int i = 0; i < md->nk; ++i) {
+            const float* k = md->h_taps.data() + ((size_t)t * md->nk_pad + i) * md->kp;
+            const int s8 = i / 8, c2 = (i % 8) / 4, e = i % 4;
+            for (int n = 0; n < mm; ++n) {
+                const float hi = tf32_rna_host(k[n]);
+                const float lo = tf32_rna_host(k[n] - hi);
+                float* dst = h.data() + (size_t)t * per_stage + (size_t)s8 * 2 * 2 * nb * 4;
+                dst[((0 * 2 + c2) * nb + n) * 4 + e] = hi;
+                dst[((1 * 2 + c2) * nb + n) * 4 + e] = lo;
+            }
+        }
+    float* d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, h.size() * sizeof(float)));
+    CUDA_TRY(cudaMemcpy(d, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+    md->d_aop = d;
+    md->aop_stage = per_stage;
+    return TNRD_OK;
+}
+
+// One stage as phi_kernel + adj_kernel.  Returns -1 when this model / launch
+// is not supported (the caller falls back to the CUDA-core kernels).
+template <int MS>
+static int launch_adj_m(const tnrd_model* md, const StageArgs& a, int batch, cudaStream_t s) {
+    using K = StageKernel<MS, true, LargeTile>;
+    using AC = adj::AdjCfg<MS>;
+    constexpr int RF = 4, TM = K::kTmTile, R = MS / 2;
+    using PC = adj::PhiCfg<MS, RF>;
+    if constexpr (!K::kPT) return -1;
+    if (!md->fast || !a.tab3 || !K::pt_fits(a)) return -1;
+    if (a.flags & (TNRD_STAGE_TOP_HALO | TNRD_STAGE_BOTTOM_HALO)) return -1;   // strips: CUDA-core kernels
+    const int pairs = (md->nk + 1) / 2;
+    const int kc = round_up((pairs + 1) / 2, 2);           // 4-filter chunks, whole K-steps of 8
+    const size_t adj_smem = AC::smem_bytes(kc);
+    if (adj_smem > 227 * 1024) return -1;
+    int rc = adj_operand(md, AC::NB, kc);
+    if (rc) return rc;
+    const int G = (a.W + AC::GW - 1) / AC::GW;
+    adj::AdjArgs q;
+    q.kc = kc;
+    q.xp = G * AC::GW + 2 * R;
+    q.phi_row = (int64_t)kc * q.xp * 4;
+    q.phi_img = (int64_t)(a.H + 2 * R) * q.phi_row;
+    q.bop = md->d_aop + (size_t)a.stage * md->aop_stage;
+    q.rows_per_cta = std::min(a.H, 128);
+    // phi workspace of this stream: as many images per pass as fit the budget
+    static const size_t budget = [] {
+        const char* e = std::getenv("TNRD_ADJ_WS_MB");
+        const long mb = e ? std::atol(e) : 4096;
+        return (size_t)std::max(64L, mb) << 20;
+    }();
+    const size_t img_bytes = (size_t)q.phi_img * sizeof(float);
+    const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)batch, budget / img_bytes));
+    const std::vector<long> key = {a.H, a.W, kc, MS};
+    float* phi = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(md->ws_mu);
+        auto& b = md->aws[s];
+        const size_t bytes = (size_t)chunk * img_bytes;
+        if (b.bytes < bytes || b.key != key) {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+            if (cs != cudaStreamCaptureStatusNone)
+                return fail(TNRD_ECUDA, "adjoint workspace must be allocated before stream capture");
+            if (b.bytes < bytes) {
+                if (b.ptr) md->retired.push_back(b.ptr);   // a captured graph may still use it
+                b.ptr = nullptr;
+                CUDA_TRY(cudaMalloc(&b.ptr, bytes));
+                b.bytes = bytes;
+            }
+            // cells no kernel writes (padding columns, all-zero filter chunks) must be finite
+            CUDA_TRY(cudaMemsetAsync(b.ptr, 0, b.bytes, s));
+            b.key = key;
+        }
+        phi = static_cast<float*>(b.ptr);
+    }
+    q.phi = phi;
+    using TB = typename K::TB;
+    auto pk = adj::phi_kernel<MS, RF, TM, TB>;
+    auto ak = adj::adj_kernel<MS>;
+    static std::mutex mu;
+    static uint64_t attr_set = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!(attr_set & (1ull << (dev & 63)))) {
+            CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+            CUDA_TRY(cudaFuncSetAttribute(ak, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            attr_set |= 1ull << (dev & 63);
+        }
+    }
+    TB tb;
+    const float* htaps = md->h_taps.data() + (size_t)a.stage * md->nk_pad * md->kp;
+    K::template fill_taps<TM, 2>(tb, htaps, a.nk);
+    const size_t phi_smem = PC::smem_bytes(a.tab3_stride);
+    for (int b0 = 0; b0 < batch; b0 += chunk) {
+        const int nb = std::min(chunk, batch - b0);
+        StageArgs c = a;
+        c.ngroups = pairs;
+        c.u_in = a.u_in + (int64_t)b0 * a.img_stride;
+        c.f = a.f + (int64_t)b0 * a.img_stride;
+        c.u_out = a.u_out + (int64_t)b0 * a.img_stride;
+        if (a.force_out) c.force_out = a.force_out + (int64_t)b0 * a.img_stride;
+        const dim3 pg((a.W + adj::kPhiTile - 1) / adj::kPhiTile, (a.H + adj::kPhiTile - 1) / adj::kPhiTile, nb);
+        pk<<<pg, adj::kPhiThreads, phi_smem, s>>>(c, q, tb);
+        CUDA_TRY(cudaGetLastError());
+        const dim3 ag(G, (a.H + q.rows_per_cta - 1) / q.rows_per_cta, nb);
+        ak<<<ag, adj::kAdjThreads, adj_smem, s>>>(c, q);
+        CUDA_TRY(cudaGetLastError());
+        g_launches.fetch_add(2);
+    }
+    return TNRD_OK;
+}
+
+static int launch_adj(const tnrd_model* md, const StageArgs& a, int batch, cudaStream_t s) {
+    switch (md->m) {
+        case 5: return launch_adj_m<5>(md, a, batch, s);
+        case 7: return launch_adj_m<7>(md, a, batch, s);
+        default: return -1;
+    }
+}
+
 static int launch_stage(const tnrd_model* md, int t, const float* u_in, const float* f,
                         float* u_out, int batch, int H, int W, int64_t ld, int64_t image_stride,
                         uint32_t flags, uint32_t* d_status, cudaStream_t s, float* force_out = nullptr) {
@@ -1722,6 +1866,10 @@ static int launch_stage(const tnrd_model* md, int t, const float* u_in, const fl
 #endif
     if (mode == 2 || mode == 5 || mode == 8)
         return fail(TNRD_EUNSUPPORTED, "tensor-core stage kernel unavailable for this model");
+    if (mode == 12) {
+        const int rc = launch_adj(md, a, batch, s);
+        if (rc != -1) return rc;   // ran (or failed); -1: unsupported here, CUDA-core kernels
+    }
     return md->fast ? dispatch_m<true>(md, a, batch, s) : dispatch_m<false>(md, a, batch, s);
 }
 
