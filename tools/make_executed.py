@@ -25,7 +25,7 @@ ex = {"_note": ("Executed work of the dominant stage kernel per pixel-stage from
       "source_hash": stamp, "libtnrd_sha1": so_hash}
 tr = {"_note": "dram__bytes_read.sum + dram__bytes_write.sum of one launch of the dominant stage kernel "
                "(ncu --set full), bytes", "source_hash": stamp}
-for cfg, name in (("c1", "c1_split"), ("c2", "c2_split"), ("c3", "c3_tile"), ("c4", "c4_tile"), ("c5", "c5_tile")):
+for cfg, name in (("c1", "c1_cluster"), ("c2", "c2_cluster"), ("c3", "c3_tile"), ("c4", "c4_tile"), ("c5", "c5_tile")):
     p = os.path.join(d, f"ncu_summary_{name}.txt")
     if not os.path.exists(p):
         continue

@@ -25,19 +25,17 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file
     python tools/prof_one.py c2 1 > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:stage_kernel_pt -s 2 -c 1 \
     -o $O/c3_tile python tools/prof_one.py c3 256 > $O/ncu_c3.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:stage_kernel_split -s 10 -c 1 \
-    -o $O/c2_split python tools/prof_one.py c2 1 > $O/ncu_c2.log 2>&1
-ncu --set full --clock-control none -k regex:stage_reduce -s 10 -c 1 \
-    -o $O/c2_reduce python tools/prof_one.py c2 1 > $O/ncu_c2r.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:stage_kernel_cl -s 10 -c 1 \
+    -o $O/c2_cluster python tools/prof_one.py c2 1 > $O/ncu_c2.log 2>&1
 ncu --set full --clock-control none -k regex:stage_kernel_pt -s 2 -c 1 \
     -o $O/c4_tile python tools/prof_one.py c4 1 > $O/ncu_c4.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:stage_kernel_pt -s 2 -c 1 \
     -o $O/c5_tile python tools/prof_one.py c5 32 > $O/ncu_c5.log 2>&1
 ncu --set full --clock-control none -k regex:stage_kernel -s 10 -c 1 \
-    -o $O/c1_split python tools/prof_one.py c1 1 > $O/ncu_c1.log 2>&1
+    -o $O/c1_cluster python tools/prof_one.py c1 1 > $O/ncu_c1.log 2>&1
 # per pixel of ONE launch: C3 / C5 launches cover half the batch (batch fork)
 PX_C3=$((128*512*512)); PX_C2=$((512*512)); PX_C4=$((16384*16384)); PX_C5=$((16*1024*1024)); PX_C1=$((256*256))
-for r in c2_split:$PX_C2 c2_reduce:$PX_C2 c3_tile:$PX_C3 c4_tile:$PX_C4 c5_tile:$PX_C5 c1_split:$PX_C1; do
+for r in c2_cluster:$PX_C2 c3_tile:$PX_C3 c4_tile:$PX_C4 c5_tile:$PX_C5 c1_cluster:$PX_C1; do
     n=${r%%:*}; px=${r#*:}
     python tools/ncu_summary.py $O/$n.ncu-rep > $O/ncu_summary_$n.txt 2>&1
     python tools/ncu_sass_stats.py $O/$n.ncu-rep $px >> $O/ncu_summary_$n.txt 2>&1
@@ -45,5 +43,5 @@ done
 python tools/launch_times.py $O/launches_c3.csv > $O/launch_times_c3.txt 2>&1
 python tools/launch_times.py $O/launches_c2.csv > $O/launch_times_c2.txt 2>&1
 python tools/make_executed.py $O > $O/executed_update.txt 2>&1
-rm -f $O/c2_reduce.ncu-rep $O/c4_tile.ncu-rep $O/c5_tile.ncu-rep $O/c1_split.ncu-rep
+rm -f $O/*.ncu-rep
 ls -la $O
