@@ -149,3 +149,18 @@ def test_parameter_space_kernels_keep_the_uniform_datapath():
         fma_ur = len(re.findall(r"\bFFMA2?\b[^;]*\bUR\d+", part))
         assert fma > 300 and fma_ur >= 0.35 * fma, (name[:80], fma, fma_ur)   # broken builds: < 2%
     assert seen >= 12, seen   # m = 3, 5, 7, 9 x tile / cluster / split
+
+
+def test_kernel_selection_setters_validate_without_a_gpu():
+    """tnrd_set_stage_kernel / tnrd_set_cluster_size are pure host state:
+    out-of-range values are rejected with TNRD_EINVAL (ValueError)."""
+    for bad in (-1, 13):
+        with pytest.raises(ValueError):
+            _lib.set_stage_kernel(bad)
+    for bad in (1, 9, -2):
+        with pytest.raises(ValueError):
+            _lib.set_cluster_size(bad)
+    for ok in (0, 2, 8, 0):
+        _lib.set_cluster_size(ok)
+    for ok in (_lib.KERNEL_CLUSTER_LARGE, _lib.KERNEL_TC_ADJOINT, _lib.KERNEL_AUTO):
+        _lib.set_stage_kernel(ok)
