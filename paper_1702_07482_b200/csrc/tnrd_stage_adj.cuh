@@ -48,8 +48,8 @@ namespace adj {
 
 constexpr int kStrips = 4;        // strips per adjoint CTA = TMEM lane quadrants = epilogue warps
 constexpr int kStripW = 32;       // pixels per strip (one warp)
-constexpr int kSlots = 5;         // phi row ring (raw phi, split in place into its tf32 hi part)
-constexpr int kLoSlots = 2;       // tf32 lo parts of the rows being multiplied
+constexpr int kSlots = 4;         // raw phi row ring (TMA destination, pixel-major)
+constexpr int kOpSlots = 2;       // A-operand buffers (tf32 hi and lo of a row, K-major core matrices)
 constexpr int kAdjThreads = 320;  // 4 epilogue warps + TMA warp + MMA warp + 4 converter warps
 constexpr int kPhiTile = 64;      // phi_kernel tile (square)
 constexpr int kPhiThreads = 256;
@@ -217,9 +217,13 @@ __global__ void __launch_bounds__(kPhiThreads, 2) phi_kernel(const StageArgs p, 
             v.y = sPhi[C::SPHI + i];
             v.z = half ? 0.0f : sPhi[2 * C::SPHI + i];
             v.w = half ? 0.0f : sPhi[3 * C::SPHI + i];
+            // chunk-major rows [y + r][kc][x + r][4]: a warp's 32 pixels are one
+            // 512 B store (a pixel-major layout, one bulk copy per row for the
+            // consumer, made this kernel 2.8x slower: 16 B stores at a 192 B stride)
             float* row = phig + (int64_t)kc * q.xp * 4;
+            const int64_t pxs = 4;
             if (!edge) {
-                *reinterpret_cast<float4*>(row + (int64_t)(Y + R) * q.phi_row + (int64_t)(X + R) * 4) = v;
+                *reinterpret_cast<float4*>(row + (int64_t)(Y + R) * q.phi_row + (int64_t)(X + R) * pxs) = v;
             } else {
                 // rows {Y, top mirror, bottom mirror} x columns {X, left, right mirror}
 #pragma unroll
@@ -230,7 +234,7 @@ __global__ void __launch_bounds__(kPhiThreads, 2) phi_kernel(const StageArgs p, 
                     for (int b = 0; b < 3; ++b) {
                         const int xb = b == 0 ? X : (b == 1 ? -1 - X : 2 * p.W - 1 - X);
                         if ((b == 1 && X >= R) || (b == 2 && X < p.W - R)) continue;
-                        *reinterpret_cast<float4*>(row + (int64_t)(ya + R) * q.phi_row + (int64_t)(xb + R) * 4) = v;
+                        *reinterpret_cast<float4*>(row + (int64_t)(ya + R) * q.phi_row + (int64_t)(xb + R) * pxs) = v;
                     }
                 }
             }
@@ -250,10 +254,17 @@ struct AdjCfg {
     static constexpr int TMEM_COLS = 2 * NB <= 32 ? 32 : (2 * NB <= 64 ? 64 : (2 * NB <= 128 ? 128 : 256));
     static constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NB >> 3) << 17) |
                                        ((uint32_t)(128 >> 4) << 24);
-    // shared layout (bytes): B | A hi [kSlots] | A lo [kLoSlots] | barriers | tmem slot
+    static constexpr int NPX = GW + 2 * R;                     // region pixels per row of the group
+    static constexpr int KCS = 128 * 16 + 16;                  // bytes between 4-filter chunks of an A
+                                                               // operand (padded: the converters'
+                                                               // chunk-strided stores spread over the banks)
+    // shared layout (bytes): B | raw [kSlots] | A hi [kOpSlots] | A lo [kOpSlots] | barriers | tmem slot
     __host__ __device__ static constexpr size_t b_bytes(int kc) { return (size_t)(kc / 2) * 2 * 2 * NB * 16; }
-    __host__ __device__ static constexpr size_t a_bytes(int kc) { return (size_t)kc * 128 * 16; }
-    static size_t smem_bytes(int kc) { return b_bytes(kc) + (kSlots + kLoSlots) * a_bytes(kc) + 256; }
+    __host__ __device__ static constexpr size_t raw_bytes(int kc) { return (size_t)NPX * kc * 16; }
+    __host__ __device__ static constexpr size_t op_bytes(int kc) { return (size_t)kc * KCS; }
+    static size_t smem_bytes(int kc) {
+        return b_bytes(kc) + kSlots * raw_bytes(kc) + 2 * kOpSlots * op_bytes(kc) + 256;
+    }
 };
 
 template <int MS>
@@ -263,15 +274,18 @@ __global__ void __launch_bounds__(kAdjThreads, 1) adj_kernel(const StageArgs p, 
     constexpr int NB = C::NB;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int KC = q.kc, KS = q.kc / 2;
-    const uint32_t abytes = (uint32_t)C::a_bytes(KC);
+    const uint32_t rawbytes = (uint32_t)C::raw_bytes(KC), opbytes = (uint32_t)C::op_bytes(KC);
     float* sB = reinterpret_cast<float*>(smem_raw);
-    unsigned char* sA = smem_raw + C::b_bytes(KC);             // hi slots, then lo slots
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (kSlots + kLoSlots) * (size_t)abytes);
-    uint64_t* full = bars;                  // [slots] TMA landed
-    uint64_t* conv = bars + kSlots;         // [slots] hi / lo split done
-    uint64_t* freea = bars + 2 * kSlots;    // [slots] MMAs that read the slot are done
-    uint64_t* accfull = bars + 3 * kSlots;  // [2] accumulator complete
-    uint64_t* accfree = accfull + 2;        // [2] accumulator read by the epilogue
+    unsigned char* sRaw = smem_raw + C::b_bytes(KC);
+    unsigned char* sHi = sRaw + (size_t)kSlots * rawbytes;
+    unsigned char* sLo = sHi + (size_t)kOpSlots * opbytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sLo + (size_t)kOpSlots * opbytes);
+    uint64_t* full = bars;                        // [kSlots] TMA landed
+    uint64_t* rawfree = bars + kSlots;            // [kSlots] converters done with the raw row
+    uint64_t* conv = bars + 2 * kSlots;           // [2] hi / lo of a row written
+    uint64_t* convfree = conv + kOpSlots;         // [2] the MMAs that read the operand buffer are done
+    uint64_t* accfull = convfree + kOpSlots;      // [2] accumulator complete
+    uint64_t* accfree = accfull + 2;              // [2] accumulator read by the epilogue
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfree + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -284,10 +298,11 @@ __global__ void __launch_bounds__(kAdjThreads, 1) adj_kernel(const StageArgs p, 
     if (tid == 0) {
         for (int i = 0; i < kSlots; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&conv[i], kStrips);
-            mbar_init(&freea[i], 1);
+            mbar_init(&rawfree[i], kStrips);
         }
         for (int i = 0; i < 2; ++i) {
+            mbar_init(&conv[i], kStrips);
+            mbar_init(&convfree[i], 1);
             mbar_init(&accfull[i], 1);
             mbar_init(&accfree[i], kStrips);
         }
@@ -314,35 +329,34 @@ __global__ void __launch_bounds__(kAdjThreads, 1) adj_kernel(const StageArgs p, 
     const float* phig = q.phi + (int64_t)img * q.phi_img;
 
     if (warp == 4) {
-        // ---- TMA producer: region row o0 + j into slot j % kSlots
+        // ---- TMA producer: region row o0 + j, columns c0 .. c0 + NPX - 1 of
+        // every 4-filter chunk (KC contiguous pieces of NPX x 16 B) into slot
+        // j % kSlots as raw[kc][px]
         if (lane == 0) {
             for (int j = 0; j < nrows; ++j) {
                 const int slot = j % kSlots;
-                if (j >= kSlots) mbar_wait(&freea[slot], ((j / kSlots) - 1) & 1);
-                mbar_expect_tx(&full[slot], abytes);
+                if (j >= kSlots) mbar_wait(&rawfree[slot], ((j / kSlots) - 1) & 1);
+                mbar_expect_tx(&full[slot], rawbytes);
                 const float* src = phig + (int64_t)(o0 + j) * q.phi_row + (int64_t)c0 * 4;
-                unsigned char* dst = sA + (size_t)slot * abytes;
+                unsigned char* dst = sRaw + (size_t)slot * rawbytes;
                 for (int kc = 0; kc < KC; ++kc)
-#pragma unroll
-                    for (int w = 0; w < kStrips; ++w)
-                        bulk_g2s(dst + ((size_t)kc * 128 + w * kStripW) * 16,
-                                 src + ((int64_t)kc * q.xp + w * C::PITCH) * 4, kStripW * 16, &full[slot]);
+                    bulk_g2s(dst + (size_t)kc * C::NPX * 16, src + (int64_t)kc * q.xp * 4, C::NPX * 16, &full[slot]);
             }
         }
     } else if (warp == 5) {
         // ---- MMA issuer: D[acc] = hi Khi + lo Khi + hi Klo over all K-steps
         if (lane == 0) {
             for (int j = 0; j < nrows; ++j) {
-                const int slot = j % kSlots, acc = j & 1;
-                mbar_wait(&conv[slot], (j / kSlots) & 1);
-                if (j >= 2) mbar_wait(&accfree[acc], ((j >> 1) - 1) & 1);
+                const int b = j & 1;
+                mbar_wait(&conv[b], (j >> 1) & 1);
+                if (j >= 2) mbar_wait(&accfree[b], ((j >> 1) - 1) & 1);
                 fence_after();
-                const uint32_t d = tmem + (uint32_t)(acc * NB);
-                const uint32_t ahi = smem_u32(sA + (size_t)slot * abytes);
-                const uint32_t alo = smem_u32(sA + (size_t)(kSlots + (j & 1)) * abytes);
+                const uint32_t d = tmem + (uint32_t)(b * NB);
+                const uint32_t ahi = smem_u32(sHi + (size_t)b * opbytes);
+                const uint32_t alo = smem_u32(sLo + (size_t)b * opbytes);
                 for (int ks = 0; ks < KS; ++ks) {
-                    const uint64_t dah = make_desc(ahi + (uint32_t)ks * 2 * 2048, 2048, 128);
-                    const uint64_t dal = make_desc(alo + (uint32_t)ks * 2 * 2048, 2048, 128);
+                    const uint64_t dah = make_desc(ahi + (uint32_t)ks * 2 * C::KCS, C::KCS, 128);
+                    const uint64_t dal = make_desc(alo + (uint32_t)ks * 2 * C::KCS, C::KCS, 128);
                     const uint32_t bb = smem_u32(sB) + (uint32_t)ks * (2 * 2 * NB * 16);
                     const uint64_t dbh = make_desc(bb, NB * 16, 128);
                     const uint64_t dbl = make_desc(bb + 2 * NB * 16, NB * 16, 128);
@@ -350,33 +364,49 @@ __global__ void __launch_bounds__(kAdjThreads, 1) adj_kernel(const StageArgs p, 
                     mma_tf32(d, dal, dbh, C::kIdesc, 1u);
                     mma_tf32(d, dah, dbl, C::kIdesc, 1u);
                 }
-                mma_commit(&freea[slot]);
-                mma_commit(&accfull[acc]);
+                mma_commit(&convfree[b]);
+                mma_commit(&accfull[b]);
             }
         }
     } else if (warp >= 6) {
-        // ---- converter warps: split row j (in place: tf32 hi) into hi + lo
-        const int ctid = tid - 6 * 32;
-        const int nconv = KC * 128 / (kStrips * 32);   // float4 per thread and row
+        // ---- converter warps: thread = region pixel px of the row; its KC
+        // float4 (4 filters each) go, split into tf32 hi and lo = phi - hi, to
+        // lane l1 of the K-major operand (strip s1 = px / PITCH, clamped) and,
+        // in the 2R columns two strips share, also to lane l2 of the strip
+        // on the left
+        const int px = tid - 6 * 32;
+        const int s1 = min(px / C::PITCH, kStrips - 1), r1 = px - C::PITCH * s1;
+        const int l1 = kStripW * s1 + r1;
+        const int l2 = (r1 < 2 * R && s1 >= 1) ? kStripW * (s1 - 1) + r1 + C::PITCH : -1;
         for (int j = 0; j < nrows; ++j) {
-            const int slot = j % kSlots;
+            const int slot = j % kSlots, b = j & 1;
             mbar_wait(&full[slot], (j / kSlots) & 1);
-            // lo buffer j & 1: its previous user, row j - 2, must have been multiplied
-            if (j >= 2) mbar_wait(&freea[(j - 2) % kSlots], ((j - 2) / kSlots) & 1);
-            float4* hi = reinterpret_cast<float4*>(sA + (size_t)slot * abytes);
-            float4* lo = reinterpret_cast<float4*>(sA + (size_t)(kSlots + (j & 1)) * abytes);
-            for (int i = 0; i < nconv; ++i) {
-                const int idx = i * (kStrips * 32) + ctid;
-                const float4 v = hi[idx];
-                float4 h, l;
-                h.x = tf32_rna(v.x); h.y = tf32_rna(v.y); h.z = tf32_rna(v.z); h.w = tf32_rna(v.w);
-                l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
-                hi[idx] = h;
-                lo[idx] = l;
+            if (j >= 2) mbar_wait(&convfree[b], ((j >> 1) - 1) & 1);   // row j - 2 multiplied
+            if (px < C::NPX) {
+                const float4* raw = reinterpret_cast<const float4*>(sRaw + (size_t)slot * rawbytes) + px;
+                unsigned char* hi = sHi + (size_t)b * opbytes;
+                unsigned char* lo = sLo + (size_t)b * opbytes;
+                for (int kc = 0; kc < KC; ++kc) {
+                    const float4 v = raw[kc * C::NPX];
+                    float4 h, l;
+                    h.x = tf32_rna(v.x); h.y = tf32_rna(v.y); h.z = tf32_rna(v.z); h.w = tf32_rna(v.w);
+                    l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
+                    const size_t o1b = (size_t)kc * C::KCS + (size_t)l1 * 16;
+                    *reinterpret_cast<float4*>(hi + o1b) = h;
+                    *reinterpret_cast<float4*>(lo + o1b) = l;
+                    if (l2 >= 0) {
+                        const size_t o2b = (size_t)kc * C::KCS + (size_t)l2 * 16;
+                        *reinterpret_cast<float4*>(hi + o2b) = h;
+                        *reinterpret_cast<float4*>(lo + o2b) = l;
+                    }
+                }
             }
             fence_async_smem();   // generic-proxy writes -> visible to the tensor core
             __syncwarp();
-            if (lane == 0) mbar_arrive(&conv[slot]);
+            if (lane == 0) {
+                mbar_arrive(&conv[b]);
+                mbar_arrive(&rawfree[slot]);
+            }
         }
     } else {
         // ---- epilogue warps: warp w = strip w = TMEM lanes 32w..
