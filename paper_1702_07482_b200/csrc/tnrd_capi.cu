@@ -1778,6 +1778,7 @@ static int launch_adj_m(const tnrd_model* md, const StageArgs& a, int batch, cud
         return (size_t)std::max(64L, mb) << 20;
     }();
     const size_t img_bytes = (size_t)q.phi_img * sizeof(float);
+    if (img_bytes > budget) return -1;   // one image's phi must fit the workspace (a 16384^2 scene: 52 GB)
     const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)batch, budget / img_bytes));
     const std::vector<long> key = {a.H, a.W, kc, MS};
     float* phi = nullptr;
