@@ -4,7 +4,7 @@ bench.py runs C3 and C5 as one tnrd_despeckle call over the whole batch in
 auto mode (the large-tile fused kernel, batch fork onto two streams) and C4
 as the whole 16384^2 scene through tnrd_plan_despeckle_host (row bands on
 their own streams, halo rows read in place).  The smaller parity cases in
-test_gpu_parity.py reach other kernels (small grids go to the split
+test_gpu_parity.py reach other kernels (small grids go to the cluster
 kernel), so these tests drive the benched launches themselves and compare
 with the float64 oracle (SURVEY 8(d) coverage table):
 
